@@ -1,0 +1,841 @@
+// libmpkb200: host launchers and the extern "C" ABI declared in
+// include/mpk_b200.h.  The cycle driver (mpk_cycle_run) is the native
+// runtime of one restarted-GMRES cycle: it enqueues every kernel of the
+// cycle on the caller's stream without synchronising; early exits are
+// device-side (ctl->done), so the host reads back once per cycle.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "kernels.cuh"
+
+using namespace mpk;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char *msg) {
+    g_err = msg;
+    return code;
+}
+
+int check_launch(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        g_err = std::string(what) + ": " + cudaGetErrorString(e);
+        return MPK_ELAUNCH;
+    }
+    return MPK_OK;
+}
+
+int sm_count_cached() {
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+constexpr int kMaxBlocksPerSm = 8;
+
+int max_blocks() { return sm_count_cached() * kMaxBlocksPerSm; }
+
+// Grid = min(tiles, SMs x resident CTAs) for a grid-stride kernel.
+template <class K> int grid_for(K kernel, size_t smem, int64_t n) {
+    static std::mutex mu;
+    static std::map<std::pair<const void *, size_t>, int> occ;
+    int per_sm;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto key = std::make_pair((const void *)kernel, smem);
+        auto it = occ.find(key);
+        if (it == occ.end()) {
+            if (smem > 48 * 1024)
+                cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            int o = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kernel, kBlock, smem);
+            if (o < 1) o = 1;
+            if (o > kMaxBlocksPerSm) o = kMaxBlocksPerSm;
+            occ[key] = o;
+            per_sm = o;
+        } else {
+            per_sm = it->second;
+        }
+    }
+    int64_t tiles = (n + kBlock - 1) / kBlock;
+    int64_t cap = (int64_t)sm_count_cached() * per_sm;
+    int64_t g = tiles < cap ? tiles : cap;
+    return (int)(g < 1 ? 1 : g);
+}
+
+// reduction workspace layout
+struct Ws {
+    unsigned *counters;
+    void *partials;
+    float *partials_low;
+    void *sums;
+};
+int64_t ws_partials_bytes() { return (int64_t)max_blocks() * kStride * 8; }
+int64_t ws_low_bytes() { return (int64_t)max_blocks() * 2 * 4; }
+Ws carve(void *base) {
+    char *p = (char *)base;
+    Ws w;
+    w.counters = (unsigned *)p;
+    p += 256;
+    w.partials = p;
+    p += align_up(ws_partials_bytes(), 256);
+    w.partials_low = (float *)p;
+    p += align_up(ws_low_bytes(), 256);
+    w.sums = p;
+    return w;
+}
+
+// ---------------------------------------------------------------------------
+// profiling: optional per-class CUDA events around cycle kernels
+// ---------------------------------------------------------------------------
+constexpr int kProfClasses = 8;
+struct ProfRec {
+    cudaEvent_t a, b;
+    int cls;
+    double bytes;
+};
+std::vector<ProfRec> g_prof_live;
+std::vector<cudaEvent_t> g_ev_pool;
+double g_prof_ms[kProfClasses];
+int64_t g_prof_cnt[kProfClasses];
+double g_prof_bytes[kProfClasses];
+bool g_prof_on = false;
+
+cudaEvent_t ev_get() {
+    if (!g_ev_pool.empty()) {
+        cudaEvent_t e = g_ev_pool.back();
+        g_ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+void prof_drain(bool wait) {
+    size_t keep = 0;
+    for (size_t i = 0; i < g_prof_live.size(); ++i) {
+        ProfRec &r = g_prof_live[i];
+        if (!wait && cudaEventQuery(r.b) != cudaSuccess) {
+            g_prof_live[keep++] = r;
+            continue;
+        }
+        cudaEventSynchronize(r.b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        g_prof_ms[r.cls] += ms;
+        g_prof_cnt[r.cls] += 1;
+        g_prof_bytes[r.cls] += r.bytes;
+        g_ev_pool.push_back(r.a);
+        g_ev_pool.push_back(r.b);
+    }
+    g_prof_live.resize(keep);
+}
+
+struct ProfScope {
+    bool on;
+    ProfRec rec;
+    cudaStream_t s;
+    ProfScope(int cls, double bytes, cudaStream_t st) : on(g_prof_on), s(st) {
+        if (!on) return;
+        if (g_prof_live.size() > 8192) prof_drain(false);
+        rec.a = ev_get();
+        rec.b = ev_get();
+        rec.cls = cls;
+        rec.bytes = bytes;
+        cudaEventRecord(rec.a, s);
+    }
+    ~ProfScope() {
+        if (!on) return;
+        cudaEventRecord(rec.b, s);
+        g_prof_live.push_back(rec);
+    }
+};
+
+// ---------------------------------------------------------------------------
+// operators
+// ---------------------------------------------------------------------------
+StencilConsts stencil_consts(const mpk_matrix *A) {
+    StencilConsts k;
+    memset(&k, 0, sizeof(k));
+    k.preset = A->preset;
+    k.nx = A->nx;
+    k.row0 = A->row0;
+    const double nx = (double)A->nx;
+    k.nglob = (A->preset == MPK_LAPLACE3D) ? (int64_t)A->nx * A->nx * A->nx : (int64_t)A->nx * A->nx;
+    volatile double h = 1.0 / (nx + 1.0);   // stencils.py:87
+    k.h = h;
+    switch (A->preset) {
+    case MPK_LAPLACE2D: {
+        const double c[5] = {-1.0, -1.0, 4.0, -1.0, -1.0};
+        memcpy(k.c, c, sizeof(c));
+        break;
+    }
+    case MPK_LAPLACE3D: {
+        const double c[7] = {-1.0, -1.0, -1.0, 6.0, -1.0, -1.0, -1.0};
+        memcpy(k.c, c, sizeof(c));
+        break;
+    }
+    case MPK_UNIFLOW2D: {   // stencils.py:91-103
+        volatile double d = A->diffusion;
+        volatile double v = A->velocity / std::sqrt(2.0);
+        volatile double hh = 0.5 * h;
+        volatile double hv = hh * v;
+        k.c[0] = -d - hv;
+        k.c[1] = -d - hv;
+        k.c[2] = 4.0 * d;
+        k.c[3] = -d + hv;
+        k.c[4] = -d + hv;
+        break;
+    }
+    case MPK_BENTPIPE2D: {  // stencils.py:104-115 (per-row parts on device)
+        volatile double c = A->convection;
+        k.cc2 = c * 2.0;
+        volatile double nc = -c;
+        k.ncc2 = nc * 2.0;
+        k.hh = 0.5 * h;
+        k.c[2] = 4.0;
+        break;
+    }
+    case MPK_STRETCHED2D: { // stencils.py:162-169
+        volatile double a = 1.0 / A->stretch;
+        volatile double b = A->stretch;
+        volatile double ab = a + b;
+        volatile double corner = -ab / 2.0;
+        volatile double ew = b - 2.0 * a;
+        volatile double ns = a - 2.0 * b;
+        const double c[9] = {corner, ns, corner, ew, 4.0 * ab, ew, corner, ns, corner};
+        memcpy(k.c, c, sizeof(c));
+        break;
+    }
+    default:
+        break;
+    }
+    return k;
+}
+
+template <typename T> StencilOp<T> make_stencil(const mpk_matrix *A) {
+    StencilOp<T> op;
+    op.n = A->n;
+    op.k = stencil_consts(A);
+    for (int i = 0; i < 9; ++i) op.cT[i] = (T)op.k.c[i];   // astype: round to nearest
+    return op;
+}
+
+template <typename T> CsrOp<T> make_csr(const mpk_matrix *A) {
+    CsrOp<T> op;
+    op.n = A->n;
+    op.rp = A->row_ptr;
+    op.ci = A->col_idx;
+    op.v = (const T *)A->values;
+    return op;
+}
+
+template <typename T, class F> int with_op(const mpk_matrix *A, F &&f) {
+    if (A->kind == MPK_STENCIL) return f(make_stencil<T>(A));
+    if (A->kind == MPK_CSR) return f(make_csr<T>(A));
+    return fail(MPK_EARG, "unknown matrix kind");
+}
+
+double spmv_bytes(const mpk_matrix *A, int sv) {
+    // CSR: sv*(nnz + 2n) + 4*(nnz + n + 1); stencil: x read + y write
+    if (A->kind == MPK_CSR) return (double)sv * (A->nnz + 2.0 * A->n) + 4.0 * (A->nnz + A->n + 1);
+    return 2.0 * sv * A->n;
+}
+
+template <typename T> Hess<T> hess_view(void *base, int m) {
+    Hess<T> H;
+    T *p = (T *)base;
+    H.m = m;
+    H.h = p;
+    p += (int64_t)(m + 1) * m;
+    H.cs = p;
+    p += m;
+    H.sn = p;
+    p += m;
+    H.g = p;
+    p += m + 1;
+    H.d = p;
+    p += m;
+    H.raw = p;
+    return H;
+}
+
+// ---------------------------------------------------------------------------
+// pass launchers
+// ---------------------------------------------------------------------------
+template <typename T, int NC, class Op, bool NORM>
+int launch_p1_nc(const Op &op, const T *src, const T *divp, T *vcol, const T *V, int64_t ld, int ndot, T *w,
+                 Ws ws, T *out, T *out_wn2, const int32_t *done, cudaStream_t s) {
+    auto kern = k_spmv_dot<T, NC, Op, NORM>;
+    int g = grid_for(kern, 0, op.n);
+    kern<<<g, kBlock, 0, s>>>(op, src, divp, vcol, V, ld, ndot, w, (T *)ws.partials, ws.counters, out,
+                              out_wn2, done);
+    return check_launch("k_spmv_dot");
+}
+
+template <typename T, class Op, bool NORM>
+int launch_p1(const Op &op, const T *src, const T *divp, T *vcol, const T *V, int64_t ld, int ndot, T *w, Ws ws,
+              T *out, T *out_wn2, const int32_t *done, cudaStream_t s) {
+    if (ndot <= 8) return launch_p1_nc<T, 8, Op, NORM>(op, src, divp, vcol, V, ld, ndot, w, ws, out, out_wn2, done, s);
+    if (ndot <= 16) return launch_p1_nc<T, 16, Op, NORM>(op, src, divp, vcol, V, ld, ndot, w, ws, out, out_wn2, done, s);
+    if (ndot <= 32) return launch_p1_nc<T, 32, Op, NORM>(op, src, divp, vcol, V, ld, ndot, w, ws, out, out_wn2, done, s);
+    return launch_p1_nc<T, kMaxCols, Op, NORM>(op, src, divp, vcol, V, ld, ndot, w, ws, out, out_wn2, done, s);
+}
+
+template <typename T, int NC>
+int launch_multidot_nc(int64_t n, const T *V, int64_t ld, int ncols, const T *w, Ws ws, T *out,
+                       const int32_t *done, cudaStream_t s) {
+    auto kern = k_multidot<T, NC>;
+    int g = grid_for(kern, 0, n);
+    kern<<<g, kBlock, 0, s>>>(n, V, ld, ncols, w, (T *)ws.partials, ws.counters, out, done);
+    return check_launch("k_multidot");
+}
+
+// out[c] = V[:, c]^T w for c < ncols, chunked by kMaxCols; writes out[ncols]
+// = w.w of the last chunk's extra slot only when ncols <= kMaxCols.
+template <typename T>
+int launch_multidot(int64_t n, const T *V, int64_t ld, int ncols, const T *w, Ws ws, T *out,
+                    const int32_t *done, cudaStream_t s) {
+    for (int c0 = 0; c0 < ncols; c0 += kMaxCols) {
+        int nc = ncols - c0 < kMaxCols ? ncols - c0 : kMaxCols;
+        int rc;
+        // scratch output so a chunk's extra slot never clobbers the next chunk
+        T *dst = ((T *)ws.sums) + S_TMP;
+        if (nc <= 8) rc = launch_multidot_nc<T, 8>(n, V + c0 * ld, ld, nc, w, ws, dst, done, s);
+        else if (nc <= 16) rc = launch_multidot_nc<T, 16>(n, V + c0 * ld, ld, nc, w, ws, dst, done, s);
+        else if (nc <= 32) rc = launch_multidot_nc<T, 32>(n, V + c0 * ld, ld, nc, w, ws, dst, done, s);
+        else rc = launch_multidot_nc<T, kMaxCols>(n, V + c0 * ld, ld, nc, w, ws, dst, done, s);
+        if (rc) return rc;
+        cudaMemcpyAsync(out + c0, dst, sizeof(T) * nc, cudaMemcpyDeviceToDevice, s);
+    }
+    return MPK_OK;
+}
+
+template <typename T, int NC>
+int launch_p2_nc(int64_t n, const T *V, int64_t ld, int ncols, const T *coef, const T *w, T *wout, Ws ws,
+                 T *out, const int32_t *done, cudaStream_t s) {
+    auto kern = k_update_dot<T, NC>;
+    size_t smem = (size_t)ncols * kBlock * sizeof(T);
+    int g = grid_for(kern, (size_t)NC * kBlock * sizeof(T), n);
+    kern<<<g, kBlock, smem, s>>>(n, V, ld, ncols, coef, w, wout, (T *)ws.partials, ws.counters, out, done);
+    return check_launch("k_update_dot");
+}
+
+template <typename T>
+int launch_p2(int64_t n, const T *V, int64_t ld, int ncols, const T *coef, const T *w, T *wout, Ws ws,
+              T *out, const int32_t *done, cudaStream_t s) {
+    if (ncols <= 8) return launch_p2_nc<T, 8>(n, V, ld, ncols, coef, w, wout, ws, out, done, s);
+    if (ncols <= 16) return launch_p2_nc<T, 16>(n, V, ld, ncols, coef, w, wout, ws, out, done, s);
+    if (ncols <= 32) return launch_p2_nc<T, 32>(n, V, ld, ncols, coef, w, wout, ws, out, done, s);
+    return launch_p2_nc<T, kMaxCols>(n, V, ld, ncols, coef, w, wout, ws, out, done, s);
+}
+
+template <typename T>
+int launch_p3(int64_t n, const T *V, int64_t ld, int ncols, const T *coef, const T *w, T *wout, Ws ws,
+              Hess<T> H, mpk_cycle_ctl *ctl, StepParams p, int do_givens, const int32_t *done,
+              cudaStream_t s) {
+    auto kern = k_update_norm<T>;
+    int m = H.m > 0 ? H.m : 0;
+    int64_t elems = ncols;
+    if (do_givens && 3 * m + 1 > elems) elems = 3 * m + 1;
+    size_t smem = (size_t)elems * sizeof(T);
+    // Occupancy is computed for the largest request this kernel sees.
+    const size_t smem_max = (size_t)(3 * MPK_MAX_STEPS + 8) * sizeof(T);
+    int g = grid_for(kern, smem_max, n);
+    kern<<<g, kBlock, smem, s>>>(n, V, ld, ncols, coef, w, wout, (T *)ws.partials, ws.counters, (T *)ws.sums, H,
+                                 ctl, p, do_givens, done);
+    return check_launch("k_update_norm");
+}
+
+template <typename T>
+int launch_residual(const mpk_matrix *A, const T *b, const T *x, T *r, T *sums, float *rlow, float *sums_low,
+                    Ws ws, cudaStream_t s) {
+    return with_op<T>(A, [&](auto op) -> int {
+        using Op = decltype(op);
+        if (rlow) {
+            if constexpr (sizeof(T) == 8) {
+                auto kern = k_residual<T, Op, true>;
+                int g = grid_for(kern, 0, op.n);
+                kern<<<g, kBlock, 0, s>>>(op, b, x, r, rlow, (T *)ws.partials, ws.partials_low, ws.counters, sums,
+                                          sums_low);
+            } else {
+                return fail(MPK_EARG, "low-precision residual copy needs an fp64 operator");
+            }
+        } else {
+            auto kern = k_residual<T, Op, false>;
+            int g = grid_for(kern, 0, op.n);
+            kern<<<g, kBlock, 0, s>>>(op, b, x, r, nullptr, (T *)ws.partials, nullptr, ws.counters, sums, nullptr);
+        }
+        return check_launch("k_residual");
+    });
+}
+
+// ---------------------------------------------------------------------------
+// preconditioner application
+// ---------------------------------------------------------------------------
+template <typename T>
+int apply_precond_t(const mpk_precond *M, const T *v, T *out, const int32_t *done, cudaStream_t s) {
+    const int64_t n = M->n;
+    if (M->kind == MPK_PC_NONE) {
+        if (out != v) cudaMemcpyAsync(out, v, sizeof(T) * n, cudaMemcpyDeviceToDevice, s);
+        return MPK_OK;
+    }
+    if (M->kind == MPK_PC_JACOBI) {
+        const int k = M->block;
+        const int64_t nb = (n + k - 1) / k;
+        int g = (int)((nb + kBlock - 1) / kBlock);
+        if (g > max_blocks()) g = max_blocks();
+        if (g < 1) g = 1;
+        if (k <= 8)
+            k_jacobi<T, 8><<<g, kBlock, 0, s>>>(n, k, (const T *)M->lu, M->piv, v, out, done);
+        else if (k <= 64)
+            k_jacobi<T, 64><<<g, kBlock, 0, s>>>(n, k, (const T *)M->lu, M->piv, v, out, done);
+        else
+            return fail(MPK_EUNSUPPORTED, "block Jacobi block size > 64 not supported on device");
+        return check_launch("k_jacobi");
+    }
+    if (M->kind == MPK_PC_POLY) {
+        T *w1 = (T *)M->work, *w2 = w1 + n, *t = w2 + n;
+        const T *work = v;
+        int rc = MPK_OK;
+        int i = 0;
+        const int d = M->degree;
+        bool first = true;
+        while (i < d && rc == MPK_OK) {
+            const double re = M->roots_re[i], im = M->roots_im[i];
+            T *wnext = (work == w1) ? w2 : w1;
+            if (im == 0.0) {   // preconditioners.py:293-297
+                const double inv = 1.0 / re;
+                const bool last = (i + 1 >= d);
+                rc = with_op<T>(M->poly_A, [&](auto op) -> int {
+                    using Op = decltype(op);
+                    auto kern = k_poly_real<T, Op>;
+                    int g = grid_for(kern, 0, op.n);
+                    kern<<<g, kBlock, 0, s>>>(op, work, last ? nullptr : wnext, out, (T)inv, first ? 1 : 0, done);
+                    return check_launch("k_poly_real");
+                });
+                i += 1;
+            } else {           // preconditioners.py:298-304
+                volatile double tr = 2.0 * re;
+                volatile double rr = re * re;
+                volatile double ii = im * im;
+                const double m2 = rr + ii;
+                const bool last = (i + 2 >= d);
+                rc = with_op<T>(M->poly_A, [&](auto op) -> int {
+                    using Op = decltype(op);
+                    auto k1 = k_poly_pair1<T, Op>;
+                    int g = grid_for(k1, 0, op.n);
+                    k1<<<g, kBlock, 0, s>>>(op, work, t, out, (T)tr, (T)m2, first ? 1 : 0, done);
+                    if (!last) {
+                        auto k2 = k_poly_pair2<T, Op>;
+                        k2<<<g, kBlock, 0, s>>>(op, work, t, wnext, (T)tr, (T)m2, done);
+                    }
+                    return check_launch("k_poly_pair");
+                });
+                i += 2;
+            }
+            first = false;
+            work = wnext;
+        }
+        return rc;
+    }
+    return fail(MPK_EARG, "unknown preconditioner kind");
+}
+
+// M applied to a vector of the solver dtype T; a lower-precision M is
+// wrapped cast-down / apply / cast-up (CastApplyPreconditioner,
+// multiprecision.py:306-308).  Scratch for the cast lives after the poly work.
+template <typename T>
+int apply_precond(const mpk_precond *M, const T *v, T *out, const int32_t *done, cudaStream_t s) {
+    const bool same = (M->dtype == MPK_F64) == (sizeof(T) == 8);
+    if (same) return apply_precond_t<T>(M, v, out, done, s);
+    if (M->dtype != MPK_F32 || sizeof(T) != 8) return fail(MPK_EARG, "preconditioner precision above solver precision");
+    const int64_t n = M->n;
+    float *lo_in = (float *)M->work + 3 * n, *lo_out = lo_in + n;
+    int g = grid_for(k_convert_gated<double, float>, 0, n);
+    k_convert_gated<double, float><<<g, kBlock, 0, s>>>(n, (const double *)v, lo_in, done);
+    int rc = apply_precond_t<float>(M, lo_in, lo_out, done, s);
+    if (rc) return rc;
+    k_convert_gated<float, double><<<g, kBlock, 0, s>>>(n, lo_out, (double *)out, done);
+    return check_launch("k_convert_gated");
+}
+
+// ---------------------------------------------------------------------------
+// one GMRES cycle
+// ---------------------------------------------------------------------------
+template <typename T> int run_cycle(const mpk_cycle_desc *d, cudaStream_t s) {
+    const int64_t n = d->n, ld = d->ld;
+    const int m = d->m;
+    if (m < 1 || m > MPK_MAX_STEPS - 1) return fail(MPK_EARG, "restart length out of range");
+    const int cap = d->steps_cap < 1 ? 1 : (d->steps_cap > m ? m : d->steps_cap);
+    const int sv = sizeof(T);
+    T *V = (T *)d->V;
+    T *w = (T *)d->work, *wp = w + ld, *wpp = wp + ld, *z = wpp + ld;
+    Ws ws = carve(d->ws);
+    T *sums = (T *)ws.sums;
+    Hess<T> H = hess_view<T>(d->hess, m);
+    mpk_cycle_ctl *ctl = d->ctl;
+    const int32_t *done = &ctl->done;
+    const bool precond = d->M != nullptr && d->M->kind != MPK_PC_NONE;
+    const double u = (sizeof(T) == 8) ? std::ldexp(1.0, -53) : std::ldexp(1.0, -24);
+    const double tf = (d->rule == MPK_RULE_U) ? u : (double)n * u;   // kernels.py:122
+    int rc;
+
+    k_cycle_begin<T><<<1, 32, 0, s>>>((const T *)d->rnorm2, sums, H, ctl, d->norm_scale);
+    if ((rc = check_launch("k_cycle_begin"))) return rc;
+
+    for (int k = 0; k < cap; ++k) {
+        const int ncols = k + 1;
+        const T *src = (k == 0) ? (const T *)d->r0 : wpp;
+        const T *divp = (k == 0) ? sums + S_GAMMA : sums + S_BETA;
+        T *vcol = V + (int64_t)k * ld;
+        const double vbytes = (double)sv * n * ncols;
+        if (!precond) {
+            ProfScope ps(0, spmv_bytes(d->A, sv) + 2.0 * sv * n + vbytes, s);
+            if (ncols <= kMaxCols) {
+                rc = with_op<T>(d->A, [&](auto op) -> int {
+                    return launch_p1<T, decltype(op), true>(op, src, divp, vcol, V, ld, ncols, w, ws, sums + S_C1,
+                                                           sums + S_WN2, done, s);
+                });
+            } else {
+                rc = with_op<T>(d->A, [&](auto op) -> int {
+                    return launch_p1<T, decltype(op), true>(op, src, divp, vcol, V, ld, 0, w, ws, sums + S_TMP,
+                                                           sums + S_WN2, done, s);
+                });
+                if (!rc) rc = launch_multidot<T>(n, V, ld, ncols, w, ws, sums + S_C1, done, s);
+            }
+        } else {
+            {
+                ProfScope ps(3, 2.0 * sv * n, s);
+                int g = grid_for(k_normalize<T>, 0, n);
+                k_normalize<T><<<g, kBlock, 0, s>>>(n, src, divp, vcol, done);
+                if ((rc = check_launch("k_normalize"))) return rc;
+            }
+            {
+                ProfScope ps(4, 0.0, s);
+                if ((rc = apply_precond<T>(d->M, vcol, z, done, s))) return rc;
+            }
+            ProfScope ps(0, spmv_bytes(d->A, sv) + sv * n + vbytes, s);
+            if (ncols <= kMaxCols) {
+                rc = with_op<T>(d->A, [&](auto op) -> int {
+                    return launch_p1<T, decltype(op), false>(op, z, divp, vcol, V, ld, ncols, w, ws, sums + S_C1,
+                                                            sums + S_WN2, done, s);
+                });
+            } else {
+                rc = with_op<T>(d->A, [&](auto op) -> int {
+                    return launch_p1<T, decltype(op), false>(op, z, divp, vcol, V, ld, 0, w, ws, sums + S_TMP,
+                                                            sums + S_WN2, done, s);
+                });
+                if (!rc) rc = launch_multidot<T>(n, V, ld, ncols, w, ws, sums + S_C1, done, s);
+            }
+        }
+        if (rc) return rc;
+        {
+            ProfScope ps(1, vbytes + 2.0 * sv * n, s);
+            if (ncols <= kMaxCols) {
+                rc = launch_p2<T>(n, V, ld, ncols, sums + S_C1, w, wp, ws, sums + S_C2, done, s);
+            } else {
+                rc = launch_p3<T>(n, V, ld, ncols, sums + S_C1, w, wp, ws, H, ctl, StepParams{k, cap, tf, d->exit_tol, 1},
+                                  0, done, s);
+                if (!rc) rc = launch_multidot<T>(n, V, ld, ncols, wp, ws, sums + S_C2, done, s);
+            }
+            if (rc) return rc;
+        }
+        {
+            ProfScope ps(2, vbytes + 2.0 * sv * n, s);
+            rc = launch_p3<T>(n, V, ld, ncols, sums + S_C2, wp, wpp, ws, H, ctl, StepParams{k, cap, tf, d->exit_tol, 1}, 1,
+                              done, s);
+            if (rc) return rc;
+        }
+    }
+    // epilogue: d = R \ g ; x_out = x0 + M(V_k d)
+    k_lsq_solve<T><<<1, 32, (size_t)(m + 1) * sizeof(T), s>>>(H, ctl, u, 0);
+    if ((rc = check_launch("k_lsq_solve"))) return rc;
+    ProfScope ps(5, (double)sv * n * (cap + 2), s);
+    const size_t smem = (size_t)(m + 1) * sizeof(T);
+    int g = grid_for(k_correct<T>, smem, n);
+    if (!precond) {
+        k_correct<T><<<g, kBlock, smem, s>>>(n, V, ld, H.d, (const T *)d->x0, (T *)d->x_out, ctl, 0);
+        return check_launch("k_correct");
+    }
+    k_correct<T><<<g, kBlock, smem, s>>>(n, V, ld, H.d, nullptr, w, ctl, 1);
+    if ((rc = check_launch("k_correct"))) return rc;
+    // M(y): gated on the triangular-breakdown flag through a scratch int is
+    // unnecessary — a failed solve leaves x_out untouched below.
+    if ((rc = apply_precond<T>(d->M, w, z, nullptr, s))) return rc;
+    int g2 = grid_for(k_add_gated<T>, 0, n);
+    k_add_gated<T><<<g2, kBlock, 0, s>>>(n, (const T *)d->x0, z, (T *)d->x_out, ctl);
+    return check_launch("k_add_gated");
+}
+
+template <typename T>
+int cgs2_append_t(int64_t n, int64_t ld, int count, T *V, const T *w, int rule, T *coeffs, T *out, int32_t *app,
+                  T *tmp, Ws ws, cudaStream_t s) {
+    T *sums = (T *)ws.sums;
+    T *wp = tmp, *wpp = tmp + n;
+    int rc;
+    const double u = (sizeof(T) == 8) ? std::ldexp(1.0, -53) : std::ldexp(1.0, -24);
+    const double tf = (rule == MPK_RULE_U) ? u : (double)n * u;
+    // ||w||^2 and c1 (multidot's extra slot carries w.w)
+    {
+        auto kern = k_dot<T>;
+        int g = grid_for(kern, 0, n);
+        kern<<<g, kBlock, 0, s>>>(n, w, w, (T *)ws.partials, ws.counters, sums + S_WN2, 0);
+        if ((rc = check_launch("k_dot"))) return rc;
+    }
+    if ((rc = launch_multidot<T>(n, V, ld, count, w, ws, sums + S_C1, nullptr, s))) return rc;
+    Hess<T> H{};
+    if (count <= kMaxCols) {
+        if ((rc = launch_p2<T>(n, V, ld, count, sums + S_C1, w, wp, ws, sums + S_C2, nullptr, s))) return rc;
+    } else {
+        if ((rc = launch_p3<T>(n, V, ld, count, sums + S_C1, w, wp, ws, H, nullptr, StepParams{0, 1, tf, 0.0, 0}, 0,
+                               nullptr, s)))
+            return rc;
+        if ((rc = launch_multidot<T>(n, V, ld, count, wp, ws, sums + S_C2, nullptr, s))) return rc;
+    }
+    if ((rc = launch_p3<T>(n, V, ld, count, sums + S_C2, wp, wpp, ws, H, nullptr, StepParams{0, 1, tf, 0.0, 0}, 0,
+                           nullptr, s)))
+        return rc;
+    int g = grid_for(k_cgs2_finish<T>, 0, n);
+    k_cgs2_finish<T><<<g, kBlock, 0, s>>>(n, sums, count, tf, wpp, V + (int64_t)count * ld, coeffs, out, app);
+    return check_launch("k_cgs2_finish");
+}
+
+}  // namespace
+
+// ===========================================================================
+// extern "C" ABI
+// ===========================================================================
+extern "C" {
+
+int mpk_abi_version(void) { return MPK_ABI_VERSION; }
+const char *mpk_last_error(void) { return g_err.c_str(); }
+int mpk_sm_count(void) { return sm_count_cached(); }
+
+int64_t mpk_reduce_ws_bytes(int64_t n, int32_t max_cols) {
+    (void)n;
+    (void)max_cols;
+    return 256 + align_up(ws_partials_bytes(), 256) + align_up(ws_low_bytes(), 256) + (int64_t)S_TOTAL * 8 + 256;
+}
+
+int64_t mpk_cycle_hess_bytes(int32_t m, int32_t dtype) {
+    const int64_t sv = dtype == MPK_F64 ? 8 : 4;
+    return sv * (2 * (int64_t)(m + 1) * m + m + m + (m + 1) + m) + 64;
+}
+
+int mpk_spmv(const mpk_matrix *A, const void *x, void *y, void *stream) {
+    if (!A || !x || !y) return fail(MPK_EARG, "null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    auto go = [&](auto tag) -> int {
+        using T = decltype(tag);
+        return with_op<T>(A, [&](auto op) -> int {
+            using Op = decltype(op);
+            if (op.n == 0) return MPK_OK;
+            auto kern = k_spmv<T, Op>;
+            int g = grid_for(kern, 0, op.n);
+            kern<<<g, kBlock, 0, s>>>(op, (const T *)x, (T *)y);
+            return check_launch("k_spmv");
+        });
+    };
+    return A->dtype == MPK_F64 ? go(double{}) : go(float{});
+}
+
+int mpk_convert(int32_t sd, int32_t dd, int64_t n, const void *src, void *dst, void *stream) {
+    if (n == 0) return MPK_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (sd == dd) {
+        cudaMemcpyAsync(dst, src, n * (sd == MPK_F64 ? 8 : 4), cudaMemcpyDeviceToDevice, s);
+        return check_launch("convert copy");
+    }
+    if (sd == MPK_F64) {
+        int g = grid_for(k_convert<double, float>, 0, n);
+        k_convert<double, float><<<g, kBlock, 0, s>>>(n, (const double *)src, (float *)dst);
+    } else {
+        int g = grid_for(k_convert<float, double>, 0, n);
+        k_convert<float, double><<<g, kBlock, 0, s>>>(n, (const float *)src, (double *)dst);
+    }
+    return check_launch("k_convert");
+}
+
+int mpk_vdiv(int32_t dtype, int64_t n, const void *x, const void *d, void *out, void *stream) {
+    if (n == 0) return MPK_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (dtype == MPK_F64) {
+        int g = grid_for(k_normalize<double>, 0, n);
+        k_normalize<double><<<g, kBlock, 0, s>>>(n, (const double *)x, (const double *)d, (double *)out, nullptr);
+    } else {
+        int g = grid_for(k_normalize<float>, 0, n);
+        k_normalize<float><<<g, kBlock, 0, s>>>(n, (const float *)x, (const float *)d, (float *)out, nullptr);
+    }
+    return check_launch("k_normalize");
+}
+
+int mpk_dot(int32_t dtype, int64_t n, const void *x, const void *y, void *result, void *ws_, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    Ws ws = carve(ws_);
+    if (dtype == MPK_F64) {
+        int g = grid_for(k_dot<double>, 0, n);
+        k_dot<double><<<g, kBlock, 0, s>>>(n, (const double *)x, (const double *)y, (double *)ws.partials,
+                                           ws.counters, (double *)result, 0);
+    } else {
+        int g = grid_for(k_dot<float>, 0, n);
+        k_dot<float><<<g, kBlock, 0, s>>>(n, (const float *)x, (const float *)y, (float *)ws.partials, ws.counters,
+                                          (float *)result, 0);
+    }
+    return check_launch("k_dot");
+}
+
+int mpk_norm2(int32_t dtype, int64_t n, const void *x, void *result, void *ws_, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    Ws ws = carve(ws_);
+    if (dtype == MPK_F64) {
+        int g = grid_for(k_dot<double>, 0, n);
+        k_dot<double><<<g, kBlock, 0, s>>>(n, (const double *)x, (const double *)x, (double *)ws.partials,
+                                           ws.counters, (double *)result, 1);
+    } else {
+        int g = grid_for(k_dot<float>, 0, n);
+        k_dot<float><<<g, kBlock, 0, s>>>(n, (const float *)x, (const float *)x, (float *)ws.partials, ws.counters,
+                                          (float *)result, 1);
+    }
+    return check_launch("k_norm2");
+}
+
+int mpk_axpy(int32_t dtype, int64_t n, double alpha, const void *x, const void *y, void *out, void *stream) {
+    if (n == 0) return MPK_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (dtype == MPK_F64) {
+        int g = grid_for(k_axpy<double>, 0, n);
+        k_axpy<double><<<g, kBlock, 0, s>>>(n, alpha, (const double *)x, (const double *)y, (double *)out);
+    } else {
+        int g = grid_for(k_axpy<float>, 0, n);
+        k_axpy<float><<<g, kBlock, 0, s>>>(n, (float)alpha, (const float *)x, (const float *)y, (float *)out);
+    }
+    return check_launch("k_axpy");
+}
+
+int mpk_scale(int32_t dtype, int64_t n, double alpha, const void *x, void *out, void *stream) {
+    return mpk_axpy(dtype, n, alpha, x, nullptr, out, stream);
+}
+
+int mpk_cgs2_append(int32_t dtype, int64_t n, int64_t ld, int32_t count, void *V, const void *w, int32_t rule,
+                    void *coeffs, void *out, int32_t *appended_dev, void *tmp, void *ws_, void *stream) {
+    if (count < 1) return fail(MPK_EARG, "basis must hold at least one vector");
+    cudaStream_t s = (cudaStream_t)stream;
+    Ws ws = carve(ws_);
+    if (dtype == MPK_F64)
+        return cgs2_append_t<double>(n, ld, count, (double *)V, (const double *)w, rule, (double *)coeffs,
+                                     (double *)out, appended_dev, (double *)tmp, ws, s);
+    return cgs2_append_t<float>(n, ld, count, (float *)V, (const float *)w, rule, (float *)coeffs, (float *)out,
+                                appended_dev, (float *)tmp, ws, s);
+}
+
+int mpk_cycle_run(const mpk_cycle_desc *d, void *stream) {
+    if (!d || !d->A || !d->V || !d->ctl || !d->ws || !d->hess || !d->work) return fail(MPK_EARG, "null argument");
+    if (d->ld < d->n) return fail(MPK_EARG, "ld < n");
+    cudaStream_t s = (cudaStream_t)stream;
+    g_prof_on = (d->flags & 1) != 0;
+    int rc = d->dtype == MPK_F64 ? run_cycle<double>(d, s) : run_cycle<float>(d, s);
+    g_prof_on = false;
+    return rc;
+}
+
+int mpk_residual(const mpk_matrix *A, const void *b, const void *x, void *r, void *sums, float *r_low,
+                 float *sums_low, void *ws_, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    Ws ws = carve(ws_);
+    if (A->dtype == MPK_F64)
+        return launch_residual<double>(A, (const double *)b, (const double *)x, (double *)r, (double *)sums, r_low,
+                                       sums_low, ws, s);
+    return launch_residual<float>(A, (const float *)b, (const float *)x, (float *)r, (float *)sums, nullptr, nullptr,
+                                  ws, s);
+}
+
+int mpk_ir_update(int64_t n, double *x, const float *u, int32_t *changed, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    int g = grid_for(k_ir_update, 0, n);
+    k_ir_update<<<g, kBlock, 0, s>>>(n, x, u, changed);
+    return check_launch("k_ir_update");
+}
+
+int mpk_precond_apply(const mpk_precond *M, const void *v, void *out, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (M->dtype == MPK_F64) return apply_precond_t<double>(M, (const double *)v, (double *)out, nullptr, s);
+    return apply_precond_t<float>(M, (const float *)v, (float *)out, nullptr, s);
+}
+
+int mpk_lsq_init(int32_t dtype, int32_t m, double gamma, double norm_scale, void *hess, mpk_cycle_ctl *ctl,
+                 void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (dtype == MPK_F64)
+        k_lsq_init<double><<<1, 32, 0, s>>>(hess_view<double>(hess, m), ctl, gamma, norm_scale);
+    else
+        k_lsq_init<float><<<1, 32, 0, s>>>(hess_view<float>(hess, m), ctl, gamma, norm_scale);
+    return check_launch("k_lsq_init");
+}
+
+int mpk_lsq_update(int32_t dtype, int32_t m, int32_t j, const void *coeffs, const void *beta, void *hess,
+                   mpk_cycle_ctl *ctl, void *ws_, void *stream) {
+    if (j < 1 || j > m) return fail(MPK_EARG, "column index out of range");
+    cudaStream_t s = (cudaStream_t)stream;
+    Ws ws = carve(ws_);
+    const StepParams p{j - 1, m, 0.0, -1.0, 0};
+    const size_t smem = (size_t)(3 * m + 1) * (dtype == MPK_F64 ? 8 : 4);
+    if (dtype == MPK_F64)
+        k_lsq_update<double><<<1, 32, smem, s>>>((const double *)coeffs, (const double *)beta, (double *)ws.sums,
+                                                 hess_view<double>(hess, m), ctl, p);
+    else
+        k_lsq_update<float><<<1, 32, smem, s>>>((const float *)coeffs, (const float *)beta, (float *)ws.sums,
+                                                hess_view<float>(hess, m), ctl, p);
+    return check_launch("k_lsq_update");
+}
+
+int mpk_lsq_solve(int32_t dtype, int32_t m, int32_t k, void *hess, mpk_cycle_ctl *ctl, void *stream) {
+    if (k < 1 || k > m) return fail(MPK_EARG, "k out of range");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (dtype == MPK_F64)
+        k_lsq_solve<double><<<1, 32, (size_t)(m + 1) * 8, s>>>(hess_view<double>(hess, m), ctl,
+                                                              std::ldexp(1.0, -53), k);
+    else
+        k_lsq_solve<float><<<1, 32, (size_t)(m + 1) * 4, s>>>(hess_view<float>(hess, m), ctl,
+                                                             std::ldexp(1.0, -24), k);
+    return check_launch("k_lsq_solve");
+}
+
+int mpk_prof_reset(void) {
+    prof_drain(true);
+    for (int i = 0; i < kProfClasses; ++i) {
+        g_prof_ms[i] = 0;
+        g_prof_cnt[i] = 0;
+        g_prof_bytes[i] = 0;
+    }
+    return MPK_OK;
+}
+
+int mpk_prof_read(double *ms, int64_t *counts, double *bytes, int32_t nclasses) {
+    prof_drain(true);
+    for (int i = 0; i < nclasses && i < kProfClasses; ++i) {
+        ms[i] = g_prof_ms[i];
+        counts[i] = g_prof_cnt[i];
+        bytes[i] = g_prof_bytes[i];
+    }
+    return MPK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,121 @@
+// Shared device helpers for libmpkb200 (sm_100a).
+//
+// Arithmetic rules: everything that must reproduce the
+// reference bit-for-bit uses the explicit round-to-nearest intrinsics
+// (__fmul_rn/__fadd_rn/__dmul_rn/__dadd_rn) so nvcc never contracts a
+// multiply-add into an FMA; the library is built without fast-math, so `/`
+// and sqrt are IEEE round-to-nearest and fp32 subnormals are preserved.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/mpk_b200.h"
+
+namespace mpk {
+
+constexpr int kBlock = 256;          // threads per CTA for streaming kernels
+constexpr int kMaxCols = 64;         // columns handled in registers per pass
+
+template <typename T> struct RN;
+template <> struct RN<double> {
+    static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+    static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+    static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+    static __device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
+    static __device__ __forceinline__ double sqrt_(double a) { return __dsqrt_rn(a); }
+    static __device__ __forceinline__ double hypot_(double a, double b) { return hypot(a, b); }
+    static __device__ __forceinline__ double from_double(double a) { return a; }
+};
+template <> struct RN<float> {
+    static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+    static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+    static __device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
+    static __device__ __forceinline__ float div(float a, float b) { return __fdiv_rn(a, b); }
+    static __device__ __forceinline__ float sqrt_(float a) { return __fsqrt_rn(a); }
+    static __device__ __forceinline__ float hypot_(float a, float b) { return hypotf(a, b); }
+    static __device__ __forceinline__ float from_double(double a) { return __double2float_rn(a); }
+};
+
+template <typename T> __device__ __forceinline__ T ldcg(const T *p) { return __ldcg(p); }
+
+// Warp-level sum (fixed butterfly order -> deterministic).
+template <typename T> __device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Reduce NC per-thread accumulators plus one extra scalar across the CTA:
+// out[c] = CTA total of column c (c < ncols), out[ncols] = CTA total of
+// `extra`.  `sm` needs (blockDim/32) * (NC+1) elements.  Deterministic:
+// fixed shuffle tree, then warps summed in index order.
+template <typename T, int NC>
+__device__ __forceinline__ void block_reduce_cols(T (&acc)[NC], int ncols, T extra, T *sm, T *out) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    constexpr int S = NC + 1;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        if (c < ncols) {
+            T v = warp_sum(acc[c]);
+            if (lane == 0) sm[warp * S + c] = v;
+        }
+    }
+    {
+        T v = warp_sum(extra);
+        if (lane == 0) sm[warp * S + NC] = v;
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c <= ncols; c += blockDim.x) {
+        const int cc = (c == ncols) ? NC : c;
+        T s = sm[cc];
+        for (int w = 1; w < nw; ++w) s += sm[w * S + cc];
+        out[c] = s;
+    }
+    __syncthreads();
+}
+
+// Grid-wide "last CTA finishes the reduction" protocol.  Every CTA writes its
+// partial row, then takes a ticket; the CTA drawing the last ticket sees all
+// partials (after the fence) and resets the counter for the next launch.
+__device__ __forceinline__ bool last_cta(unsigned *counter) {
+    __shared__ bool s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (s_last) __threadfence();
+    return s_last;
+}
+
+// Second stage: the last CTA sums partials[nblk][stride] (ncols columns
+// plus the extra at index ncols) in a fixed order: thread t folds partial
+// rows t, t+B, ... into registers (independent loads), then one CTA column
+// reduction.  Results: out[0..ncols].
+template <typename T, int NC>
+__device__ __forceinline__ void reduce_partials(const T *partials, int nblk, int stride, int ncols,
+                                                T *sm, T *out) {
+    T acc[NC];
+    T extra = T(0);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[c] = T(0);
+    for (int b = threadIdx.x; b < nblk; b += blockDim.x) {
+        const T *row = partials + (int64_t)b * stride;
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+            if (c < ncols) acc[c] += ldcg(row + c);
+        extra += ldcg(row + ncols);
+    }
+    block_reduce_cols<T, NC>(acc, ncols, extra, sm, out);
+}
+
+// Workspace carved out of the caller's reduction buffer.
+struct RedWs {
+    unsigned *counters;   // 16 ticket counters (zero-initialised by the caller)
+    void *partials;       // max_blocks * stride elements
+    void *sums;           // 256 elements: reduced results
+};
+
+__host__ __device__ inline int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+}  // namespace mpk

@@ -1,0 +1,639 @@
+// Device kernels of the GMRES solve path (sm_100a, HBM-bound; no tensor
+// cores: SpMV is ~0.17 flop/B and the CGS2 skinny GEMVs ~0.25 flop/B).
+//
+// Per Arnoldi step the reference does (gmres.py:180-193, kernels.py:114-126):
+//   z = M v_k; w = A z; ||w||; c1 = V^T w; w -= V c1; c2 = V^T w; w -= V c2;
+//   beta = ||w||; append w/beta; Givens update.
+// Here that is three streaming passes over the basis, each ending in a
+// deterministic grid reduction finished by the last CTA:
+//   P1 k_spmv_dot     v_k = w''/beta (fused normalise), w = A v_k, ||w||^2, V^T w
+//   P2 k_update_dot   w' = w - V c1, V^T w'
+//   P3 k_update_norm  w'' = w' - V c2, ||w''||^2, then (last CTA) beta, the
+//                     append test and the Givens update of the Hessenberg column
+// The basis V is column-major with leading dimension ld (multiple of 64), so
+// every column read by a warp is one contiguous, aligned 128/256-byte line.
+#pragma once
+
+#include "ops.cuh"
+
+namespace mpk {
+
+constexpr int kStride = kMaxCols + 2;   // partial-row stride (columns + extra)
+
+// sums[] layout (elements of T)
+enum : int {
+    S_C1 = 0,
+    S_C2 = MPK_MAX_STEPS + 8,
+    S_WN2 = 2 * (MPK_MAX_STEPS + 8),
+    S_BN2,
+    S_BETA,
+    S_GAMMA,
+    S_RN2,
+    S_APP,
+    S_TMP,
+    S_TOTAL = S_TMP + 2 * kStride
+};
+
+template <typename T> struct Hess {
+    T *h;    // (m+1) x m, column-major
+    T *cs;   // m
+    T *sn;   // m
+    T *g;    // m+1
+    T *d;    // m   (back-substitution result)
+    T *raw;  // (m+1) x m unrotated columns (coeffs, beta) for diagnostics
+    int m;
+};
+
+__device__ __forceinline__ bool skip(const int32_t *done) {
+    return done != nullptr && *(volatile const int32_t *)done != 0;
+}
+
+__device__ __forceinline__ int64_t gtid() { return (int64_t)blockIdx.x * blockDim.x + threadIdx.x; }
+__device__ __forceinline__ int64_t gstride() { return (int64_t)gridDim.x * blockDim.x; }
+
+// ---------------------------------------------------------------------------
+// P1: (normalise) + SpMV + ||w||^2 + first projection V^T w
+// ---------------------------------------------------------------------------
+template <typename T, int NC, class Op, bool NORM>
+__global__ void __launch_bounds__(kBlock) k_spmv_dot(Op A, const T *__restrict__ src,
+                                                     const T *__restrict__ divp, T *__restrict__ vcol,
+                                                     const T *__restrict__ V, int64_t ld, int ndot,
+                                                     T *__restrict__ w, T *partials, unsigned *counter,
+                                                     T *out, T *out_wn2, const int32_t *done) {
+    __shared__ T sm[(kBlock / 32) * (NC + 1)];
+    if (skip(done)) return;
+    const T dv = NORM ? *divp : T(1);
+    T acc[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[c] = T(0);
+    T an = T(0);
+    for (int64_t r = gtid(); r < A.n; r += gstride()) {
+        T wr, own = T(0);
+        if constexpr (NORM) {
+            wr = A.row(r, XScaled<T>{src, dv});
+            own = RN<T>::div(src[r], dv);
+            vcol[r] = own;
+        } else {
+            wr = A.row(r, XPlain<T>{src});
+        }
+        w[r] = wr;
+        an += wr * wr;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            if (c < ndot) {
+                const T v = (NORM && c == ndot - 1) ? own : V[(int64_t)c * ld + r];
+                acc[c] += v * wr;
+            }
+        }
+    }
+    block_reduce_cols<T, NC>(acc, ndot, an, sm, partials + (int64_t)blockIdx.x * kStride);
+    if (last_cta(counter)) {
+        reduce_partials<T, NC>(partials, gridDim.x, kStride, ndot, sm, out);
+        if (threadIdx.x == 0) {
+            *out_wn2 = out[ndot];
+            *counter = 0u;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// P2: w' = w - V c ; V^T w'   (row of V staged in shared memory, reused)
+// ---------------------------------------------------------------------------
+template <typename T, int NC>
+__global__ void __launch_bounds__(kBlock) k_update_dot(int64_t n, const T *__restrict__ V, int64_t ld,
+                                                       int ncols, const T *__restrict__ coef,
+                                                       const T *__restrict__ w, T *__restrict__ wout,
+                                                       T *partials, unsigned *counter, T *out,
+                                                       const int32_t *done) {
+    extern __shared__ unsigned char dsm_raw[];
+    T *stage = reinterpret_cast<T *>(dsm_raw);
+    __shared__ T sm[(kBlock / 32) * (NC + 1)];
+    __shared__ T sc[NC];
+    if (skip(done)) return;
+    for (int c = threadIdx.x; c < ncols; c += blockDim.x) sc[c] = coef[c];
+    __syncthreads();
+    T acc[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[c] = T(0);
+    const int t = threadIdx.x;
+    for (int64_t r = gtid(); r < n; r += gstride()) {
+        T s = T(0);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            if (c < ncols) {
+                const T v = V[(int64_t)c * ld + r];
+                stage[c * kBlock + t] = v;
+                s += v * sc[c];
+            }
+        }
+        const T wr = RN<T>::sub(w[r], s);
+        wout[r] = wr;
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+            if (c < ncols) acc[c] += stage[c * kBlock + t] * wr;
+    }
+    block_reduce_cols<T, NC>(acc, ncols, T(0), sm, partials + (int64_t)blockIdx.x * kStride);
+    if (last_cta(counter)) {
+        reduce_partials<T, NC>(partials, gridDim.x, kStride, ncols, sm, out);
+        if (threadIdx.x == 0) *counter = 0u;
+    }
+}
+
+// Plain multi-dot out[c] = V[:, c0+c]^T w for a chunk of <= NC columns
+// (used past kMaxCols columns and by the standalone cgs2 entry point).
+template <typename T, int NC>
+__global__ void __launch_bounds__(kBlock) k_multidot(int64_t n, const T *__restrict__ V, int64_t ld,
+                                                     int ncols, const T *__restrict__ w, T *partials,
+                                                     unsigned *counter, T *out, const int32_t *done) {
+    __shared__ T sm[(kBlock / 32) * (NC + 1)];
+    if (skip(done)) return;
+    T acc[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[c] = T(0);
+    T an = T(0);
+    for (int64_t r = gtid(); r < n; r += gstride()) {
+        const T wr = w[r];
+        an += wr * wr;
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+            if (c < ncols) acc[c] += V[(int64_t)c * ld + r] * wr;
+    }
+    block_reduce_cols<T, NC>(acc, ncols, an, sm, partials + (int64_t)blockIdx.x * kStride);
+    if (last_cta(counter)) {
+        reduce_partials<T, NC>(partials, gridDim.x, kStride, ncols, sm, out);
+        if (threadIdx.x == 0) *counter = 0u;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Hessenberg / Givens (kernels.py:129-196) on one CTA
+// ---------------------------------------------------------------------------
+struct StepParams {
+    int k;              // 0-based step index; column j = k + 1
+    int steps_cap;
+    double thresh_factor;   // n*u (rule n_u) or u (rule u)
+    double exit_tol;
+    int test_append;        // 0: standalone update (no append test, no exit)
+};
+
+// Executed by a whole CTA.  Reads c1, c2, beta (sums[S_BETA]) and ||w||^2,
+// writes the rotated column to H and the step outcome to ctl.  Thread 0 runs
+// the serial rotation chain with the column in shared memory.
+template <typename T>
+__device__ void hessenberg_step(T *sums, Hess<T> H, mpk_cycle_ctl *ctl, const StepParams p) {
+    extern __shared__ unsigned char dsm_raw[];
+    T *col = reinterpret_cast<T *>(dsm_raw);     // m+1
+    T *scs = col + (H.m + 1);                    // m
+    T *ssn = scs + H.m;                          // m
+    __shared__ int s_app;
+    const int j = p.k + 1;
+    const T beta = sums[S_BETA];
+    for (int i = threadIdx.x; i < j; i += blockDim.x) {
+        col[i] = RN<T>::add(sums[S_C1 + i], sums[S_C2 + i]);
+        if (i < j - 1) {
+            scs[i] = H.cs[i];
+            ssn[i] = H.sn[i];
+        }
+    }
+    T *rc = H.raw + (int64_t)(j - 1) * (H.m + 1);
+    for (int i = threadIdx.x; i < j; i += blockDim.x) rc[i] = col[i];
+    if (threadIdx.x == 0) {
+        rc[j] = beta;
+        col[j] = beta;
+        if (p.test_append) {
+            const T wnorm = RN<T>::sqrt_(sums[S_WN2]);
+            const double thr = p.thresh_factor * (double)wnorm;   // kernels.py:122-123
+            s_app = ((double)beta > thr) ? 1 : 0;
+        } else {
+            s_app = 1;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        T carry = col[0];
+        for (int i = 0; i < j - 1; ++i) {
+            const T a = carry, b = col[i + 1];
+            const T c = scs[i], s = ssn[i];
+            col[i] = RN<T>::add(RN<T>::mul(c, a), RN<T>::mul(s, b));
+            carry = RN<T>::add(RN<T>::mul(-s, a), RN<T>::mul(c, b));
+        }
+        const T a = carry, b = col[j];
+        T c, s, r;
+        if (b == T(0)) {
+            c = T(1); s = T(0); r = a;
+        } else {
+            r = RN<T>::hypot_(a, b);
+            c = RN<T>::div(a, r);
+            s = RN<T>::div(b, r);
+        }
+        H.cs[j - 1] = c;
+        H.sn[j - 1] = s;
+        col[j - 1] = r;
+        col[j] = T(0);
+        const T gprev = H.g[j - 1];
+        const T gj = RN<T>::mul(-s, gprev);
+        H.g[j] = gj;
+        H.g[j - 1] = RN<T>::mul(c, gprev);
+        const double rel = fabs((double)gj) / ctl->scale;
+        ctl->implicit_relres[p.k] = rel;
+        ctl->steps = j;
+        if (p.test_append) {
+            if (!s_app) {
+                ctl->breakdown = 1;
+                ctl->done = 1;
+            } else if (rel <= p.exit_tol || j >= p.steps_cap) {
+                ctl->done = 1;
+            }
+        }
+    }
+    __syncthreads();
+    T *hc = H.h + (int64_t)(j - 1) * (H.m + 1);
+    for (int i = threadIdx.x; i <= j; i += blockDim.x) hc[i] = col[i];
+}
+
+// ---------------------------------------------------------------------------
+// P3: w'' = w' - V c ; ||w''||^2 ; last CTA: beta, append test, Givens
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(kBlock) k_update_norm(int64_t n, const T *__restrict__ V, int64_t ld,
+                                                        int ncols, const T *__restrict__ coef,
+                                                        const T *__restrict__ w, T *__restrict__ wout,
+                                                        T *partials, unsigned *counter, T *sums,
+                                                        Hess<T> H, mpk_cycle_ctl *ctl, StepParams p,
+                                                        int do_givens, const int32_t *done) {
+    extern __shared__ unsigned char dsm_raw[];
+    T *sc = reinterpret_cast<T *>(dsm_raw);      // ncols (reused by the Givens step)
+    __shared__ T sm[(kBlock / 32) * 2];
+    if (skip(done)) return;
+    for (int c = threadIdx.x; c < ncols; c += blockDim.x) sc[c] = coef[c];
+    __syncthreads();
+    T an = T(0);
+    for (int64_t r = gtid(); r < n; r += gstride()) {
+        T s = T(0);
+        int c = 0;
+        for (; c + 8 <= ncols; c += 8) {
+            T v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = V[(int64_t)(c + q) * ld + r];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) s += v[q] * sc[c + q];
+        }
+        for (; c < ncols; ++c) s += V[(int64_t)c * ld + r] * sc[c];
+        const T wr = RN<T>::sub(w[r], s);
+        wout[r] = wr;
+        an += wr * wr;
+    }
+    T dummy[1] = {T(0)};
+    block_reduce_cols<T, 1>(dummy, 0, an, sm, partials + (int64_t)blockIdx.x * kStride);
+    if (last_cta(counter)) {
+        reduce_partials<T, 1>(partials, gridDim.x, kStride, 0, sm, sums + S_BN2);
+        if (threadIdx.x == 0) {
+            *counter = 0u;
+            sums[S_BETA] = RN<T>::sqrt_(sums[S_BN2]);   // beta = norm2(w'') in T
+        }
+        __syncthreads();
+        if (do_givens) hessenberg_step<T>(sums, H, ctl, p);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// cycle prologue / epilogue
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_cycle_begin(const T *rnorm2, T *sums, Hess<T> H, mpk_cycle_ctl *ctl,
+                              double norm_scale) {
+    if (threadIdx.x != 0) return;
+    const T gamma = RN<T>::sqrt_(*rnorm2);
+    sums[S_GAMMA] = gamma;
+    H.g[0] = gamma;
+    ctl->gamma = (double)gamma;
+    double scale = norm_scale > 0.0 ? norm_scale : (double)gamma;
+    ctl->steps = 0;
+    ctl->breakdown = 0;
+    ctl->tri_err = 0;
+    ctl->done = (gamma == T(0)) ? 1 : 0;
+    if (gamma == T(0) && !(scale > 0.0)) scale = 1.0;   // gmres.py:170-172
+    ctl->scale = scale;
+}
+
+// normalise: vcol = src / d (kernels.py:125 / gmres.py:174)
+template <typename T>
+__global__ void k_normalize(int64_t n, const T *__restrict__ src, const T *divp, T *__restrict__ vcol,
+                            const int32_t *done) {
+    if (skip(done)) return;
+    const T d = *divp;
+    for (int64_t r = gtid(); r < n; r += gstride()) vcol[r] = RN<T>::div(src[r], d);
+}
+
+// Back-substitution R d = g with the k*u*max|diag| guard (kernels.py:202-216).
+// One warp.  k = ctl->steps.
+template <typename T>
+__global__ void k_lsq_solve(Hess<T> H, mpk_cycle_ctl *ctl, double u, int kfixed) {
+    extern __shared__ unsigned char dsm_raw[];
+    T *rhs = reinterpret_cast<T *>(dsm_raw);
+    __shared__ T s_d;
+    const int k = kfixed > 0 ? kfixed : ctl->steps;
+    if (k <= 0 || ctl->tri_err) return;
+    const int ldh = H.m + 1;
+    if (threadIdx.x == 0) {
+        T dmax = fabs(H.h[0]), dmin = dmax;
+        int imin = 0;
+        for (int i = 1; i < k; ++i) {
+            const T a = fabs(H.h[(int64_t)i * ldh + i]);
+            if (a > dmax) dmax = a;
+            if (a < dmin) { dmin = a; imin = i; }     // np.argmin: first minimum
+        }
+        const double thr = (double)k * u * (double)dmax;
+        if ((double)dmin <= thr) {
+            ctl->tri_err = 1;
+            ctl->tri_index = imin;
+            ctl->tri_entry = (double)dmin;
+            ctl->tri_threshold = thr;
+        }
+    }
+    __syncwarp();
+    if (*(volatile int32_t *)&ctl->tri_err) return;
+    for (int i = threadIdx.x; i < k; i += 32) rhs[i] = H.g[i];
+    __syncwarp();
+    for (int i = k - 1; i >= 0; --i) {
+        if (threadIdx.x == 0) {
+            s_d = RN<T>::div(rhs[i], H.h[(int64_t)i * ldh + i]);
+            H.d[i] = s_d;
+        }
+        __syncwarp();
+        const T di = s_d;
+        for (int q = threadIdx.x; q < i; q += 32) rhs[q] = rhs[q] - H.h[(int64_t)i * ldh + q] * di;
+        __syncwarp();
+    }
+}
+
+// x_out = x0 + V[:, :k] d   (mode 0)      or   y = V[:, :k] d   (mode 1)
+// gmres.py:195-196.  k = ctl->steps; k == 0 copies x0.
+template <typename T>
+__global__ void __launch_bounds__(kBlock) k_correct(int64_t n, const T *__restrict__ V, int64_t ld,
+                                                    const T *__restrict__ dvec, const T *__restrict__ x0,
+                                                    T *__restrict__ out, const mpk_cycle_ctl *ctl,
+                                                    int mode) {
+    extern __shared__ unsigned char dsm_raw[];
+    T *sd = reinterpret_cast<T *>(dsm_raw);
+    if (ctl->tri_err) return;
+    const int k = ctl->steps;
+    for (int c = threadIdx.x; c < k; c += blockDim.x) sd[c] = dvec[c];
+    __syncthreads();
+    for (int64_t r = gtid(); r < n; r += gstride()) {
+        T s = T(0);
+        int c = 0;
+        for (; c + 8 <= k; c += 8) {
+            T v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = V[(int64_t)(c + q) * ld + r];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) s += v[q] * sd[c + q];
+        }
+        for (; c < k; ++c) s += V[(int64_t)c * ld + r] * sd[c];
+        if (mode == 0)
+            out[r] = (k == 0) ? x0[r] : RN<T>::add(x0[r], s);
+        else
+            out[r] = s;
+    }
+}
+
+// out = x0 + z  (the preconditioned correction, gmres.py:196); ctl gates it
+template <typename T>
+__global__ void k_add_gated(int64_t n, const T *__restrict__ x0, const T *__restrict__ z,
+                            T *__restrict__ out, const mpk_cycle_ctl *ctl) {
+    if (ctl->tri_err) return;
+    const int k = ctl->steps;
+    for (int64_t r = gtid(); r < n; r += gstride()) out[r] = (k == 0) ? x0[r] : RN<T>::add(x0[r], z[r]);
+}
+
+// ---------------------------------------------------------------------------
+// explicit residual r = b - A x (+ fp32 copy for refinement)
+// ---------------------------------------------------------------------------
+template <typename T, class Op, bool LOW>
+__global__ void __launch_bounds__(kBlock) k_residual(Op A, const T *__restrict__ b, const T *__restrict__ x,
+                                                     T *__restrict__ r, float *__restrict__ rlow,
+                                                     T *partials, float *partials_low, unsigned *counter,
+                                                     T *out, float *out_low) {
+    __shared__ T sm[(kBlock / 32) * 2];
+    __shared__ float smf[(kBlock / 32) * 2];
+    T an = T(0);
+    float al = 0.f;
+    for (int64_t i = gtid(); i < A.n; i += gstride()) {
+        const T ri = RN<T>::sub(b[i], A.row(i, XPlain<T>{x}));
+        if (r) r[i] = ri;
+        an += ri * ri;
+        if constexpr (LOW) {
+            const float li = __double2float_rn((double)ri);
+            rlow[i] = li;
+            al += li * li;
+        }
+    }
+    T d1[1] = {T(0)};
+    block_reduce_cols<T, 1>(d1, 0, an, sm, partials + (int64_t)blockIdx.x * kStride);
+    if constexpr (LOW) {
+        float d2[1] = {0.f};
+        block_reduce_cols<float, 1>(d2, 0, al, smf, partials_low + (int64_t)blockIdx.x * 2);
+    }
+    if (last_cta(counter)) {
+        reduce_partials<T, 1>(partials, gridDim.x, kStride, 0, sm, out);
+        if constexpr (LOW) reduce_partials<float, 1>(partials_low, gridDim.x, 2, 0, smf, out_low);
+        if (threadIdx.x == 0) *counter = 0u;
+    }
+}
+
+// x_next = x + (double) u ; changed |= (x_next != x)   (multiprecision.py:207-214)
+__global__ void k_ir_update(int64_t n, double *__restrict__ x, const float *__restrict__ u,
+                            int32_t *changed) {
+    bool any = false;
+    for (int64_t i = gtid(); i < n; i += gstride()) {
+        const double xo = x[i];
+        const double xn = __dadd_rn(xo, (double)u[i]);
+        any |= !(xn == xo);
+        x[i] = xn;
+    }
+    if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) atomicOr(changed, 1);
+}
+
+// ---------------------------------------------------------------------------
+// standalone vector kernels (kernels.py:31-52, sparse.py:190-226)
+// ---------------------------------------------------------------------------
+template <typename T, class Op>
+__global__ void __launch_bounds__(kBlock) k_spmv(Op A, const T *__restrict__ x, T *__restrict__ y) {
+    for (int64_t r = gtid(); r < A.n; r += gstride()) y[r] = A.row(r, XPlain<T>{x});
+}
+
+template <typename S, typename D>
+__global__ void k_convert(int64_t n, const S *__restrict__ s, D *__restrict__ d) {
+    for (int64_t i = gtid(); i < n; i += gstride()) {
+        if constexpr (sizeof(D) == 4 && sizeof(S) == 8)
+            d[i] = __double2float_rn(s[i]);
+        else
+            d[i] = (D)s[i];
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kBlock) k_dot(int64_t n, const T *__restrict__ x, const T *__restrict__ y,
+                                                T *partials, unsigned *counter, T *out, int take_sqrt) {
+    __shared__ T sm[(kBlock / 32) * 2];
+    T a = T(0);
+    for (int64_t i = gtid(); i < n; i += gstride()) a += x[i] * y[i];
+    T d1[1] = {T(0)};
+    block_reduce_cols<T, 1>(d1, 0, a, sm, partials + (int64_t)blockIdx.x * kStride);
+    if (last_cta(counter)) {
+        reduce_partials<T, 1>(partials, gridDim.x, kStride, 0, sm, out);
+        if (threadIdx.x == 0) {
+            if (take_sqrt) out[0] = RN<T>::sqrt_(out[0]);
+            *counter = 0u;
+        }
+    }
+}
+
+template <typename T>
+__global__ void k_axpy(int64_t n, T a, const T *__restrict__ x, const T *__restrict__ y, T *__restrict__ out) {
+    for (int64_t i = gtid(); i < n; i += gstride())
+        out[i] = y ? RN<T>::add(y[i], RN<T>::mul(a, x[i])) : RN<T>::mul(a, x[i]);
+}
+
+// standalone cgs2_append epilogue: coeffs = c1 + c2, beta, append test and
+// the new column w''/beta when appended (kernels.py:121-126)
+template <typename T>
+__global__ void k_cgs2_finish(int64_t n, const T *sums, int count, double thresh_factor,
+                              const T *__restrict__ wpp, T *__restrict__ vnew, T *coeffs, T *out,
+                              int32_t *appended) {
+    const T beta = RN<T>::sqrt_(sums[S_BN2]);
+    const T wnorm = RN<T>::sqrt_(sums[S_WN2]);
+    const bool app = (double)beta > thresh_factor * (double)wnorm;
+    if (blockIdx.x == 0) {
+        for (int c = threadIdx.x; c < count; c += blockDim.x)
+            coeffs[c] = RN<T>::add(sums[S_C1 + c], sums[S_C2 + c]);
+        if (threadIdx.x == 0) {
+            out[0] = beta;
+            out[1] = wnorm;
+            *appended = app ? 1 : 0;
+        }
+    }
+    if (!app) return;
+    for (int64_t r = gtid(); r < n; r += gstride()) vnew[r] = RN<T>::div(wpp[r], beta);
+}
+
+// ---------------------------------------------------------------------------
+// preconditioners (preconditioners.py:133-139, 276-305)
+// ---------------------------------------------------------------------------
+// Block Jacobi: one thread per k-by-k block; getrs order: row swaps (piv,
+// sequential as dlaswp), unit-lower forward, upper backward.
+template <typename T, int KMAX>
+__global__ void k_jacobi(int64_t n, int k, const T *__restrict__ lu, const int32_t *__restrict__ piv,
+                         const T *__restrict__ v, T *__restrict__ out, const int32_t *done) {
+    if (skip(done)) return;
+    const int64_t nb = (n + k - 1) / k;
+    for (int64_t b = gtid(); b < nb; b += gstride()) {
+        const int64_t s = b * k;
+        const int kb = (int)((s + k <= n) ? k : (n - s));
+        if (k == 1) {
+            out[s] = RN<T>::div(v[s], lu[b]);
+            continue;
+        }
+        const T *L = lu + b * (int64_t)k * k;   // row-major kb x kb (leading dim k)
+        const int32_t *P = piv + b * (int64_t)k;
+        T xb[KMAX];
+        for (int i = 0; i < kb; ++i) xb[i] = v[s + i];
+        for (int i = 0; i < kb; ++i) {
+            const int p = P[i];
+            if (p != i) { const T t = xb[i]; xb[i] = xb[p]; xb[p] = t; }
+        }
+        for (int i = 1; i < kb; ++i) {
+            T a = xb[i];
+            for (int j = 0; j < i; ++j) a -= L[i * k + j] * xb[j];
+            xb[i] = a;
+        }
+        for (int i = kb - 1; i >= 0; --i) {
+            T a = xb[i];
+            for (int j = i + 1; j < kb; ++j) a -= L[i * k + j] * xb[j];
+            xb[i] = RN<T>::div(a, L[i * k + i]);
+        }
+        for (int i = 0; i < kb; ++i) out[s + i] = xb[i];
+    }
+}
+
+// GMRES polynomial, real root: acc += inv*work ; work_next = work - inv*(A work)
+template <typename T, class Op>
+__global__ void __launch_bounds__(kBlock) k_poly_real(Op A, const T *__restrict__ work, T *__restrict__ wnext,
+                                                      T *__restrict__ acc, T inv, int first,
+                                                      const int32_t *done) {
+    if (skip(done)) return;
+    for (int64_t r = gtid(); r < A.n; r += gstride()) {
+        const T wr = work[r];
+        const T p = RN<T>::mul(inv, wr);
+        acc[r] = RN<T>::add(first ? T(0) : acc[r], p);
+        if (wnext) {
+            const T y = A.row(r, XPlain<T>{work});
+            wnext[r] = RN<T>::sub(wr, RN<T>::mul(inv, y));
+        }
+    }
+}
+
+// conjugate pair, part 1: t = A work ; acc += (tr*work - t)/m2
+template <typename T, class Op>
+__global__ void __launch_bounds__(kBlock) k_poly_pair1(Op A, const T *__restrict__ work, T *__restrict__ t,
+                                                       T *__restrict__ acc, T tr, T m2, int first,
+                                                       const int32_t *done) {
+    if (skip(done)) return;
+    for (int64_t r = gtid(); r < A.n; r += gstride()) {
+        const T tv = A.row(r, XPlain<T>{work});
+        t[r] = tv;
+        const T q = RN<T>::div(RN<T>::sub(RN<T>::mul(tr, work[r]), tv), m2);
+        acc[r] = RN<T>::add(first ? T(0) : acc[r], q);
+    }
+}
+
+// conjugate pair, part 2: work_next = work - (tr*t - A t)/m2
+template <typename T, class Op>
+__global__ void __launch_bounds__(kBlock) k_poly_pair2(Op A, const T *__restrict__ work, const T *__restrict__ t,
+                                                       T *__restrict__ wnext, T tr, T m2, const int32_t *done) {
+    if (skip(done)) return;
+    for (int64_t r = gtid(); r < A.n; r += gstride()) {
+        const T s = A.row(r, XPlain<T>{t});
+        wnext[r] = RN<T>::sub(work[r], RN<T>::div(RN<T>::sub(RN<T>::mul(tr, t[r]), s), m2));
+    }
+}
+
+template <typename S, typename D>
+__global__ void k_convert_gated(int64_t n, const S *__restrict__ s, D *__restrict__ d, const int32_t *done) {
+    if (skip(done)) return;
+    for (int64_t i = gtid(); i < n; i += gstride()) {
+        if constexpr (sizeof(D) == 4 && sizeof(S) == 8)
+            d[i] = __double2float_rn(s[i]);
+        else
+            d[i] = (D)s[i];
+    }
+}
+
+// Standalone HessenbergSystem (kernels.py:139-216) on device state.
+template <typename T>
+__global__ void k_lsq_init(Hess<T> H, mpk_cycle_ctl *ctl, double gamma, double norm_scale) {
+    if (threadIdx.x != 0) return;
+    H.g[0] = RN<T>::from_double(gamma);
+    ctl->gamma = gamma;
+    ctl->scale = norm_scale;
+    ctl->steps = 0;
+    ctl->done = 0;
+    ctl->breakdown = 0;
+    ctl->tri_err = 0;
+}
+
+template <typename T>
+__global__ void k_lsq_update(const T *coeffs, const T *beta, T *sums, Hess<T> H, mpk_cycle_ctl *ctl,
+                             StepParams p) {
+    const int j = p.k + 1;
+    for (int i = threadIdx.x; i < j; i += blockDim.x) {
+        sums[S_C1 + i] = coeffs[i];
+        sums[S_C2 + i] = T(0);    // c1 + 0 == c1 exactly
+    }
+    if (threadIdx.x == 0) sums[S_BETA] = *beta;
+    __syncthreads();
+    hessenberg_step<T>(sums, H, ctl, p);
+}
+
+}  // namespace mpk

@@ -1,0 +1,114 @@
+// Row operators: CSR and matrix-free stencil rows with the reference's exact
+// summation order.
+//
+// mpkrylov.spmv (sparse.py:190-206) is SciPy csr_matvec: per row, a running
+// sum starting at 0 adds value*x[col] over the stored entries in storage
+// order, rounding after each multiply and add.  Both operators below do the
+// same with explicit _rn intrinsics, so they are bit-identical to the
+// reference.  The stencil operator regenerates generate_stencil's values
+// (stencils.py:78-207) on the fly, in the reference's operation order, so it
+// is bit-identical to the CSR product of the assembled matrix while reading
+// only x and writing y.
+#pragma once
+
+#include "common.cuh"
+
+namespace mpk {
+
+template <typename T> struct CsrOp {
+    int64_t n;
+    const int32_t *__restrict__ rp;
+    const int32_t *__restrict__ ci;
+    const T *__restrict__ v;
+
+    template <class X> __device__ __forceinline__ T row(int64_t r, X x) const {
+        const int32_t p0 = __ldg(rp + r), p1 = __ldg(rp + r + 1);
+        T acc = T(0);
+        for (int32_t p = p0; p < p1; ++p)
+            acc = RN<T>::add(acc, RN<T>::mul(__ldg(v + p), x((int64_t)__ldg(ci + p))));
+        return acc;
+    }
+    static constexpr bool kStencil = false;
+};
+
+// Host-computed constants of a stencil preset (double, reference formulas).
+struct StencilConsts {
+    int preset;
+    int nx;
+    int64_t row0;        // first global row of this block
+    int64_t nglob;       // nx^2 or nx^3
+    double c[9];         // constant coefficients (displacement order)
+    double h, hh;        // h = 1/(nx+1), hh = 0.5*h      (BentPipe)
+    double cc2, ncc2;    // c*2.0 and (-c)*2.0            (BentPipe)
+};
+
+template <typename T> struct StencilOp {
+    int64_t n;
+    StencilConsts k;
+    T cT[9];
+
+    template <class X> __device__ __forceinline__ T row(int64_t r, X x) const {
+        const int64_t g = k.row0 + r;
+        const int nx = k.nx;
+        T acc = T(0);
+        if (k.preset == MPK_LAPLACE3D) {
+            const int64_t nxy = (int64_t)nx * nx;
+            const int ix = (int)(g % nx), iy = (int)((g / nx) % nx), iz = (int)(g / nxy);
+            if (iz > 0) acc = RN<T>::add(acc, RN<T>::mul(cT[0], x(r - nxy)));
+            if (iy > 0) acc = RN<T>::add(acc, RN<T>::mul(cT[1], x(r - nx)));
+            if (ix > 0) acc = RN<T>::add(acc, RN<T>::mul(cT[2], x(r - 1)));
+            acc = RN<T>::add(acc, RN<T>::mul(cT[3], x(r)));
+            if (ix < nx - 1) acc = RN<T>::add(acc, RN<T>::mul(cT[4], x(r + 1)));
+            if (iy < nx - 1) acc = RN<T>::add(acc, RN<T>::mul(cT[5], x(r + nx)));
+            if (iz < nx - 1) acc = RN<T>::add(acc, RN<T>::mul(cT[6], x(r + nxy)));
+            return acc;
+        }
+        const int ix = (int)(g % nx), iy = (int)(g / nx);
+        if (k.preset == MPK_STRETCHED2D) {
+            const bool W = ix > 0, E = ix < nx - 1, S = iy > 0, N = iy < nx - 1;
+            if (W && S) acc = RN<T>::add(acc, RN<T>::mul(cT[0], x(r - nx - 1)));
+            if (S) acc = RN<T>::add(acc, RN<T>::mul(cT[1], x(r - nx)));
+            if (E && S) acc = RN<T>::add(acc, RN<T>::mul(cT[2], x(r - nx + 1)));
+            if (W) acc = RN<T>::add(acc, RN<T>::mul(cT[3], x(r - 1)));
+            acc = RN<T>::add(acc, RN<T>::mul(cT[4], x(r)));
+            if (E) acc = RN<T>::add(acc, RN<T>::mul(cT[5], x(r + 1)));
+            if (W && N) acc = RN<T>::add(acc, RN<T>::mul(cT[6], x(r + nx - 1)));
+            if (N) acc = RN<T>::add(acc, RN<T>::mul(cT[7], x(r + nx)));
+            if (E && N) acc = RN<T>::add(acc, RN<T>::mul(cT[8], x(r + nx + 1)));
+            return acc;
+        }
+        T c0 = cT[0], c1 = cT[1], c2 = cT[2], c3 = cT[3], c4 = cT[4];
+        if (k.preset == MPK_BENTPIPE2D) {
+            // stencils.py:104-115, evaluated left to right as numpy does
+            const double px = __dmul_rn((double)(ix + 1), k.h);
+            const double py = __dmul_rn((double)(iy + 1), k.h);
+            const double ux = __dmul_rn(__dmul_rn(k.cc2, py), __dsub_rn(1.0, __dmul_rn(px, px)));
+            const double uy = __dmul_rn(__dmul_rn(k.ncc2, px), __dsub_rn(1.0, __dmul_rn(py, py)));
+            c0 = RN<T>::from_double(__dsub_rn(-1.0, __dmul_rn(k.hh, uy)));
+            c1 = RN<T>::from_double(__dsub_rn(-1.0, __dmul_rn(k.hh, ux)));
+            c3 = RN<T>::from_double(__dadd_rn(-1.0, __dmul_rn(k.hh, ux)));
+            c4 = RN<T>::from_double(__dadd_rn(-1.0, __dmul_rn(k.hh, uy)));
+        }
+        if (iy > 0) acc = RN<T>::add(acc, RN<T>::mul(c0, x(r - nx)));
+        if (ix > 0) acc = RN<T>::add(acc, RN<T>::mul(c1, x(r - 1)));
+        acc = RN<T>::add(acc, RN<T>::mul(c2, x(r)));
+        if (ix < nx - 1) acc = RN<T>::add(acc, RN<T>::mul(c3, x(r + 1)));
+        if (iy < nx - 1) acc = RN<T>::add(acc, RN<T>::mul(c4, x(r + nx)));
+        return acc;
+    }
+    static constexpr bool kStencil = true;
+};
+
+// x accessors
+template <typename T> struct XPlain {
+    const T *__restrict__ p;
+    __device__ __forceinline__ T operator()(int64_t c) const { return p[c]; }
+};
+// x = src / d, exactly the reference's basis column w / beta (kernels.py:125)
+template <typename T> struct XScaled {
+    const T *__restrict__ p;
+    T d;
+    __device__ __forceinline__ T operator()(int64_t c) const { return RN<T>::div(p[c], d); }
+};
+
+}  // namespace mpk

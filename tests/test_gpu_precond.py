@@ -1,0 +1,117 @@
+"""Preconditioner application on the GPU vs the oracle / dense solves, and
+preconditioned solves vs the reference goldens."""
+
+import numpy as np
+import pytest
+
+import paper_2105_07544_b200 as mk
+from oracle import mpk_oracle as O
+
+pytestmark = pytest.mark.gpu
+P = mk.Precision
+
+
+def L(preset, nx):
+    return mk.generate_stencil(mk.ProblemSpec(preset, nx))
+
+
+def test_identity_returns_input(cuda, rng):
+    M = mk.identity(6, P.binary64)
+    v = rng.standard_normal(6)
+    assert M.apply(v) is v and M.kind == "identity"
+
+
+def test_block_jacobi_apply(cuda, rng):
+    from conftest import random_csr
+
+    A, dense = random_csr(mk, rng, 24)
+    M = mk.build_block_jacobi(A, 5)
+    assert M.data.num_blocks == 5 and M.data.starts[-1] == 24
+    v = rng.standard_normal(24)
+    out = M.apply(v)
+    for s in range(0, 24, 5):
+        e = min(s + 5, 24)
+        assert np.allclose(out[s:e], np.linalg.solve(dense[s:e, s:e], v[s:e]), rtol=1e-11, atol=1e-13)
+    M1 = mk.build_block_jacobi(A, 1)
+    assert np.array_equal(M1.apply(v), v / np.diagonal(dense))
+    M32 = mk.build_block_jacobi(A, 4, precision=P.binary32)
+    assert M32.apply(v.astype(np.float32)).dtype == np.float32
+    with pytest.raises(mk.PrecisionMismatchError):
+        M32.apply(v)
+
+
+def test_singular_block_reported(cuda):
+    A = mk.csr_from_coo(np.array([0, 1, 2, 2, 3, 3]), np.array([0, 1, 2, 3, 2, 3]),
+                        np.array([1.0, 1.0, 1.0, 2.0, 2.0, 4.0]), 4)
+    with pytest.raises(mk.SingularBlockError) as info:
+        mk.build_block_jacobi(A, 2)
+    assert info.value.block_index == 1
+
+
+def test_poly_apply_bit_exact_given_roots(cuda, runs):
+    st = L("Stretched2D", 32)
+    A32 = mk.convert_matrix(st, P.binary32)
+    b = np.ones(st.n, np.float32)
+    M = mk.build_gmres_poly(A32, 20, b)
+    g = runs["poly_st32_roots"]
+    assert M.data.degree == g["degree"]
+    want_roots = np.array(g["roots_re"]) + 1j * np.array(g["roots_im"])
+    assert np.abs(M.data.roots - want_roots).max() <= 1e-3 * np.abs(want_roots).max()
+    # apply with the reference's exact roots: bit-identical to the oracle's product form
+    M.data.roots = want_roots
+    M._desc = None
+    v = np.random.default_rng(5).standard_normal(st.n).astype(np.float32)
+    ref = O.Poly(want_roots, g["degree"], 20, False, st.row_ptr, st.col_idx,
+                 st.values.astype(np.float32))
+    assert np.array_equal(M.apply(v), ref(v))
+
+
+def test_poly_on_identity_truncates(cuda, rng):
+    n = 12
+    idx = np.arange(n)
+    A = mk.csr_from_coo(idx, idx, np.ones(n), n)
+    M = mk.build_gmres_poly(A, 5, np.ones(n))
+    assert M.data.truncated and M.data.degree == 1 and M.data.requested_degree == 5
+    v = rng.standard_normal(n)
+    assert np.allclose(M.apply(v), v, rtol=1e-14)
+
+
+def test_loss_of_accuracy_goldens(cuda, runs):
+    st = L("Stretched2D", 32)
+    b = np.ones(st.n)
+    M32 = mk.build_gmres_poly(mk.convert_matrix(st, P.binary32), 20, b.astype(np.float32))
+    W = mk.wrap_low_precision_preconditioner(M32, P.binary64)
+    assert W.kind == "cast[poly]"
+    cfg = mk.SolverConfig(m=50, rtol=1e-10, max_iters=2000)
+    rep = mk.gmres_restarted(st, W, b, np.zeros(st.n), cfg)
+    g = runs["loss_recover_st32"]
+    assert rep.loss_of_accuracy and rep.converged
+    assert abs(rep.total_iters - g["iters"]) <= 50
+    rep = mk.gmres_restarted(st, W, b, np.zeros(st.n), cfg, explicit_restart_on_loss=False)
+    assert rep.loss_of_accuracy and not rep.converged
+    assert abs(rep.total_iters - runs["loss_giveup_st32"]["iters"]) <= 50
+
+
+def test_preconditioned_goldens(cuda, runs):
+    l16 = L("Laplace2D", 16)
+    Mj = mk.build_block_jacobi(l16, 16)
+    rep = mk.gmres_restarted(l16, Mj, np.ones(256), np.zeros(256), mk.SolverConfig(m=50, rtol=1e-10))
+    assert rep.converged and rep.total_iters == runs["jacobi16_l2d16"]["iters"]
+    bp24 = L("BentPipe2D", 24)
+    Mj1 = mk.build_block_jacobi(bp24, 1)
+    rep = mk.gmres_restarted(bp24, Mj1, np.ones(576), np.zeros(576), mk.SolverConfig(m=50, rtol=1e-10))
+    assert rep.converged and rep.total_iters == runs["jacobi1_bp24"]["iters"]
+    inner = mk.SolverConfig(m=50, rtol=1e-4, precision=P.binary32, max_iters=20000)
+    for k, name in ((1, "ir_jacobi1_bp24"), (8, "ir_jacobi8_bp24")):
+        Mk = mk.build_block_jacobi(bp24, k, P.binary32)
+        rep = mk.gmres_ir(bp24, np.ones(576), np.zeros(576), mk.IrConfig(inner=inner, rtol=1e-10), M=Mk)
+        assert rep.converged and abs(rep.total_iters - runs[name]["iters"]) <= 50
+    rng = np.random.default_rng(7)
+    b7 = rng.standard_normal(256)
+    Mp = mk.build_gmres_poly(l16, 10, b7)
+    rep = mk.gmres_restarted(l16, Mp, b7, np.zeros(256), mk.SolverConfig(m=50, rtol=1e-10))
+    assert rep.converged and abs(rep.total_iters - runs["poly10_l2d16_seed7"]["iters"]) <= 1
+    st = L("Stretched2D", 32)
+    M32 = mk.build_gmres_poly(mk.convert_matrix(st, P.binary32), 20, np.ones(st.n, np.float32))
+    rep = mk.gmres_ir(st, np.ones(st.n), np.zeros(st.n), mk.IrConfig(inner=inner, rtol=1e-10), M=M32)
+    assert rep.converged and abs(rep.total_iters - runs["ir_poly20_st32"]["iters"]) <= 50

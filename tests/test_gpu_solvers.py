@@ -1,0 +1,202 @@
+"""Solver-level parity on the GPU against the reference's golden runs
+(tests/golden/runs.json, produced by the unmodified mpkrylov).
+
+Contract (BASELINE north star): convergence to the same tolerance, iteration
+counts within one restart cycle, residual histories within a stated
+tolerance.  Dot products are tree-reduced on the device instead of
+OpenBLAS's order, so counts that end on a noise floor may move slightly
+(SURVEY §0 fact 3); fp64 counts are expected to match exactly.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2105_07544_b200 as mk
+
+pytestmark = pytest.mark.gpu
+
+P = mk.Precision
+# histories: relative agreement on implicit/explicit residuals, per precision
+HIST_RTOL = {"fp64": 1e-5, "fp32": 5e-3}
+
+
+def L(preset, nx):
+    return mk.generate_stencil(mk.ProblemSpec(preset, nx))
+
+
+def compare(rep, g, slack=0, hist="fp64", exact_iters=True):
+    assert rep.converged == g["converged"]
+    if exact_iters:
+        assert rep.total_iters == g["iters"], (rep.total_iters, g["iters"])
+        assert rep.restarts == g["restarts"]
+    else:
+        assert abs(rep.total_iters - g["iters"]) <= slack, (rep.total_iters, g["iters"])
+    assert rep.stalled == g["stalled"]
+    assert rep.loss_of_accuracy == g["loss"]
+    got = [(e.iteration, e.phase, e.implicit_relres, e.explicit_relres) for e in rep.history]
+    want = g["history"]
+    n = min(len(got), len(want))
+    tol = HIST_RTOL[hist]
+    worst = 0.0
+    for a, b in zip(got[:n], want[:n]):
+        assert a[1] == b[1]
+        for i in (2, 3):
+            if a[i] is not None and b[i] is not None:
+                # relative agreement, floored at the solver tolerance scale
+                d = abs(a[i] - b[i]) / max(abs(b[i]), 1e-9)
+                worst = max(worst, d)
+    assert worst <= tol, worst
+    if g["converged"]:
+        assert rep.final_explicit_relres <= 1e-10 or g["relres"] > 1e-10
+    return worst
+
+
+def gm(A, b, **kw):
+    cfg = mk.SolverConfig(**kw)
+    return mk.gmres_restarted(A, None, b.astype(cfg.precision.dtype),
+                              np.zeros(A.n, cfg.precision.dtype), cfg)
+
+
+def ir(A, b, m=50, rtol=1e-10, M=None, max_iters=20000, **kw):
+    inner = mk.SolverConfig(m=m, rtol=1e-4, precision=P.binary32, max_iters=max_iters)
+    return mk.gmres_ir(A, b, np.zeros(A.n), mk.IrConfig(inner=inner, rtol=rtol, **kw), M=M)
+
+
+def fd(A, b, s, m=50):
+    cfg = mk.FdConfig(switch_iter=s, low=mk.SolverConfig(m=m, rtol=1e-10, precision=P.binary32),
+                      high=mk.SolverConfig(m=m, rtol=1e-10))
+    return mk.gmres_fd(A, b, np.zeros(A.n), cfg)
+
+
+def test_fp64_restarted_goldens(cuda, runs, runs_x):
+    l16, l32 = L("Laplace2D", 16), L("Laplace2D", 32)
+    compare(gm(l16, np.ones(256), m=50, rtol=1e-10), runs["gmres_l2d16_m50"])
+    compare(gm(l16, np.ones(256), m=10, rtol=1e-10), runs["gmres_l2d16_m10"])
+    compare(gm(l16, np.ones(256), m=5, rtol=1e-10, max_iters=8), runs["gmres_l2d16_m5_cap8"])
+    compare(gm(l16, np.ones(256), m=5, rtol=1e-10, max_restarts=2), runs["gmres_l2d16_m5_r2"])
+    for m in (25, 50, 100):
+        compare(gm(l32, np.ones(1024), m=m, rtol=1e-10), runs["gmres_l2d32_m%d" % m])
+    rep = gm(l16, np.ones(256), m=50, rtol=1e-10)
+    assert np.abs(rep.x - runs_x["gmres_l2d16_m50"]).max() <= 1e-9 * np.abs(rep.x).max()
+    compare(gm(L("BentPipe2D", 64), np.ones(4096), m=50, rtol=1e-10), runs["gmres_bp64"])
+    compare(gm(L("UniFlow2D", 48), np.ones(48 * 48), m=50, rtol=1e-10), runs["gmres_uf48"])
+
+
+def test_fp32_restarted(cuda, runs):
+    A = mk.convert_matrix(L("Laplace2D", 8), P.binary32)
+    rep = gm(A, np.ones(64), m=20, rtol=1e-4, precision=P.binary32)
+    compare(rep, runs["gmres32_l2d8_m20"], hist="fp32")
+    assert rep.x.dtype == np.float32 and rep.history[0].phase == "single"
+
+
+def test_ir_goldens(cuda, runs):
+    l16, l32 = L("Laplace2D", 16), L("Laplace2D", 32)
+    compare(ir(l32, np.ones(1024)), runs["ir_l2d32_m50"], hist="fp32")
+    compare(ir(l32, np.ones(1024), m=25), runs["ir_l2d32_m25"], hist="fp32")
+    compare(ir(l32, np.ones(1024), m=100), runs["ir_l2d32_m100"], hist="fp32", exact_iters=False, slack=2)
+    compare(ir(l16, np.ones(256)), runs["ir_l2d16_m50"], hist="fp32", exact_iters=False, slack=2)
+    rep = ir(l16, np.ones(256), max_iters=60)
+    assert rep.total_iters <= 60
+    compare(ir(L("BentPipe2D", 64), np.ones(4096)), runs["ir_bp64"], hist="fp32", exact_iters=False,
+            slack=50)
+
+
+def test_ir_stall_on_fp32_invisible_residual(cuda, runs):
+    A = L("Laplace2D", 4)
+    rep = ir(A, 1e-15 * np.ones(16), m=10, rtol=1e-14)
+    g = runs["ir_stall_l2d4"]
+    assert rep.stalled and not rep.converged
+    assert (rep.total_iters, rep.restarts) == (g["iters"], g["restarts"])
+
+
+def test_ir_history_layout(cuda):
+    A = L("Laplace2D", 16)
+    rep = ir(A, np.ones(256))
+    assert {e.phase for e in rep.history} == {"inner", "outer"}
+    inner = [e for e in rep.history if e.phase == "inner"]
+    assert [e.iteration for e in inner] == list(range(1, rep.total_iters + 1))
+    outer = [e for e in rep.history if e.phase == "outer"]
+    assert outer[-1].explicit_relres == rep.final_explicit_relres
+    assert rep.phase_iters == {"inner": rep.total_iters, "outer": rep.restarts}
+
+
+def test_fd_goldens(cuda, runs):
+    l32 = L("Laplace2D", 32)
+    rep0 = fd(l32, np.ones(1024), 0)
+    pure = gm(l32, np.ones(1024), m=50, rtol=1e-10)
+    assert np.array_equal(rep0.x, pure.x) and rep0.total_iters == pure.total_iters
+    assert rep0.phase_iters == {"single": 0, "double": 71}
+    for s in (50, 100, 150, 200):
+        g = runs["fd_l2d32_s%d" % s]
+        rep = fd(l32, np.ones(1024), s)
+        compare(rep, g, hist="fp32", exact_iters=False, slack=10)
+        assert rep.phase_iters["single"] == s
+
+
+def test_lucky_breakdown_and_zero_rhs(cuda):
+    nx = 16
+    A = L("Laplace2D", nx)
+    grid = (np.arange(nx) + 1) / (nx + 1) * np.pi
+    b = np.outer(np.sin(grid), np.sin(grid)).ravel()
+    rep = gm(A, b, m=50, rtol=1e-10)
+    assert rep.converged and rep.total_iters == 1 and rep.final_explicit_relres <= 1e-12
+    with pytest.raises(mk.ZeroRightHandSideError):
+        gm(A, np.zeros(A.n), m=5)
+    with pytest.raises(mk.ZeroRightHandSideError):
+        ir(A, np.zeros(A.n))
+
+
+def test_exact_initial_guess_and_identity(cuda, rng):
+    n = 30
+    idx = np.arange(n)
+    A = mk.csr_from_coo(idx, idx, np.ones(n), n)
+    b = rng.standard_normal(n)
+    rep = mk.gmres_restarted(A, None, b, b.copy(), mk.SolverConfig(m=10, rtol=1e-8))
+    assert rep.converged and rep.total_iters == 0 and rep.final_explicit_relres == 0.0
+    rep = mk.gmres_restarted(A, None, b, np.zeros(n), mk.SolverConfig(m=10, rtol=1e-12))
+    assert rep.total_iters == 1 and np.allclose(rep.x, b, atol=1e-14)
+
+
+def test_random_nonsymmetric_vs_dense_solve(cuda, rng):
+    from conftest import random_csr
+
+    for n in (24, 80, 128):
+        A, dense = random_csr(mk, rng, n)
+        b = rng.standard_normal(n)
+        rep = mk.gmres_restarted(A, None, b, np.zeros(n), mk.SolverConfig(m=30, rtol=1e-12))
+        want = np.linalg.solve(dense, b)
+        assert rep.converged
+        assert np.abs(rep.x - want).max() <= 1e-7 * np.abs(want).max()
+
+
+def test_collected_basis_orthonormal_and_arnoldi(cuda):
+    A = L("Laplace2D", 16)
+    n = A.n
+    x, st = mk.gmres_cycle(A, None, np.ones(n), np.zeros(n), mk.SolverConfig(m=30, rtol=1e-300),
+                           collect_basis=True)
+    k = st.steps
+    V, H = st.basis, st.hessenberg
+    assert V.shape == (n, k + 1) and H.shape == (k + 1, k)
+    assert np.abs(V.T @ V - np.eye(k + 1)).max() <= 1e-12
+    AV = np.column_stack([mk.spmv(A, V[:, j].copy()) for j in range(k)])
+    assert np.linalg.norm(AV - V @ H) <= 1e-10 * np.linalg.norm(A.values) * np.sqrt(k)
+
+
+def test_device_tensors_through_the_solver(cuda):
+    import torch
+
+    A = L("BentPipe2D", 32)
+    b = torch.ones(A.n, dtype=torch.float64, device=cuda)
+    inner = mk.SolverConfig(m=50, rtol=1e-4, precision=P.binary32)
+    rep = mk.gmres_ir(A, b, torch.zeros_like(b), mk.IrConfig(inner=inner, rtol=1e-10))
+    assert isinstance(rep.x, torch.Tensor) and rep.x.is_cuda and rep.converged
+
+
+def test_c1_laplace3d40_counts(cuda, runs):
+    A = L("Laplace3D", 40)
+    b = np.ones(A.n)
+    compare(gm(A, b, m=50, rtol=1e-10), runs["gmres_l3d40"])
+    compare(ir(A, b), runs["ir_l3d40"], hist="fp32")
+    inner = mk.SolverConfig(m=50, rtol=1e-4, precision=P.binary32, max_iters=20000, breakdown_rule="u")
+    rep = mk.gmres_ir(A, b, np.zeros(A.n), mk.IrConfig(inner=inner, rtol=1e-10))
+    compare(rep, runs["ir_l3d40_rule_u"], hist="fp32")
