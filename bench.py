@@ -1,0 +1,302 @@
+"""Benchmark: GMRES-IR time-to-1e-10 on BASELINE config C2 (BentPipe2D 1500^2,
+2.25M rows, restart 50, fp32 inner / fp64 outer), with the fp64 GMRES time,
+per-kernel HBM roofline and the reference CPU path (oracle port) beside it.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config C2|C1|C4] [--no-fp64] [--no-cpu]
+
+A step = one full solve (b = ones, x0 = 0, m = 50, rtol 1e-10) with inputs
+resident in HBM (value); e2e repeats it through the public API with host
+(pinned) b/x0 and the solution copied back.  Working set (Krylov basis
+459 MB fp32 / 918 MB fp64) exceeds the 126 MB L2, so no explicit flush.
+N > 1: one independent replica per rank ("replicas only" for now; the
+row-partitioned solver is paper_2105_07544_b200.distributed), max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "C1": ("Laplace3D", 40, "Laplace3D 7-point 40^3 (64k rows)"),
+    "C2": ("BentPipe2D", 1500, "BentPipe2D convection-diffusion 1500^2 (2.25M rows)"),
+    "C4": ("Laplace3D", 200, "Laplace3D 7-point 200^3 (8M rows)"),
+}
+# reference (mpkrylov) iteration counts on these configs (tests/golden/runs.json)
+REF_ITERS = {"C1": {"ir": 200, "fp64": 206}, "C2": {"ir": 10650, "fp64": 10833},
+             "C4": {"ir": None, "fp64": 4053}}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), \
+        int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_sample(cfg_name, solver, steps_budget=50):
+    """Oracle port (CPU restatement of the reference) on a bounded sample:
+    `steps_budget` inner iterations of the same workload; returns s/iteration."""
+    from oracle import mpk_oracle as O
+
+    preset, nx, _ = CONFIGS[cfg_name]
+    rp, ci, v = O.stencil_csr(preset, nx)
+    n = rp.size - 1
+    b = np.ones(n)
+    t0 = time.perf_counter()
+    if solver == "ir":
+        out = O.refine((rp, ci, v), b, np.zeros(n), 50, 1e-10, steps_budget,
+                       A32=(rp, ci, v.astype(np.float32)))
+    else:
+        out = O.restarted((rp, ci, v), None, b, np.zeros(n), 50, 1e-10, steps_budget)
+    dt = time.perf_counter() - t0
+    return dt / max(out.iters, 1), out.iters, dt
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    preset, nx, desc = CONFIGS[args.config]
+    iters_full = REF_ITERS[args.config]["ir"] or REF_ITERS[args.config]["fp64"]
+    for _ in range(args.warmup):
+        cpu_sample(args.config, "ir", 10)
+    per_it = []
+    for _ in range(args.steps):
+        s, it, _dt = cpu_sample(args.config, "ir", 50)
+        per_it.append(s)
+    value = float(np.median(per_it)) * iters_full
+    line = {
+        "impl": "reference", "metric": "GMRES-IR time-to-1e-10 residual (s)", "value": value,
+        "unit": "s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32-inner/f64-outer", "data": "synthetic (generated stencil, b = ones)",
+        "config": {"workload": "%s GMRES-IR(50) rtol 1e-10" % desc, "config": args.config},
+        "cpu_baseline": {"value": value, "unit": "s", "cores": cpu_cores(), "kind": "port",
+                         "sample": "50 inner iterations (one refinement) of the same solve per step, "
+                                   "median s/iteration x reference iteration count %d" % iters_full},
+        "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-fp64", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2105_07544_b200 as mk
+    from paper_2105_07544_b200 import _lib
+
+    lib = _lib.load()
+    P = mk.Precision
+    preset, nx, desc = CONFIGS[args.config]
+    A = mk.generate_stencil(mk.ProblemSpec(preset, nx))
+    A_low = mk.convert_matrix(A, P.binary32)
+    n = A.n
+    inner = mk.SolverConfig(m=50, rtol=1e-4, precision=P.binary32, max_iters=100000)
+    icfg = mk.IrConfig(inner=inner, rtol=1e-10)
+    b_dev = torch.ones(n, dtype=torch.float64, device="cuda")
+    x0_dev = torch.zeros(n, dtype=torch.float64, device="cuda")
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    def timed(fn, steps):
+        """CUDA-event time of `steps` back-to-back calls, max over ranks (ms)."""
+        barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        reps = [fn() for _ in range(steps)]
+        ev1.record()
+        barrier()
+        ms = ev0.elapsed_time(ev1)
+        if world > 1:
+            t = torch.tensor([ms], device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, reps
+
+    solve_ir = lambda: mk.gmres_ir(A, b_dev, x0_dev, icfg, A_low=A_low)  # noqa: E731
+    for _ in range(args.warmup):
+        rep = solve_ir()
+    # timed region: K solves with per-kernel events on the launching stream
+    launches0 = lib.mpk_launch_count()
+    lib.mpk_prof_reset()
+    from paper_2105_07544_b200.engine import CycleWorkspace
+
+    wsi = CycleWorkspace.get(n, 50, P.binary32)
+    wsi.flags = 1
+    with ClockSampler(local) as clk:
+        ms_ir, reps = timed(solve_ir, args.steps)
+    wsi.flags = 0
+    launches = lib.mpk_launch_count() - launches0
+    NC = 8
+    pm = (ctypes_arr := __import__("ctypes").c_double * NC)()
+    pc = (__import__("ctypes").c_int64 * NC)()
+    pb = ctypes_arr()
+    lib.mpk_prof_read(pm, pc, pb, NC)
+    rep = reps[-1]
+    ms_step = ms_ir / args.steps
+    names = ["spmv+norm+dot1", "update1+dot2", "update2+norm+givens", "normalise", "precond",
+             "correction", "residual", "other"]
+    kern = {}
+    for i in range(NC):
+        if pc[i]:
+            kern[names[i]] = {"ms_total": pm[i], "launches": int(pc[i]),
+                              "alg_GBs": pb[i] / (pm[i] * 1e-3) / 1e9 if pm[i] > 0 else None}
+    top = max(range(NC), key=lambda i: pm[i])
+    peak, peak_kind = peaks()
+    achieved = pb[top] / (pm[top] * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "traffic_%s.json" % args.config)
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(names[top])
+        except Exception:
+            traffic = None
+
+    out = {
+        "metric": "GMRES-IR time-to-1e-10 residual (s)",
+        "value": ms_step / 1e3,
+        "unit": "s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32-inner/f64-outer",
+        "data": "synthetic (generated %s, b = ones, x0 = 0)" % preset,
+        "config": {"workload": "%s, GMRES-IR restart 50, rtol 1e-10, 1 B200 per rank" % desc,
+                   "config": args.config, "n": n, "nnz": A.nnz, "m": 50,
+                   "operator": "matrix-free stencil (bit-identical to CSR)",
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "working set > L2 (basis %.0f MB)" % ((51 * n * 4) / 1e6)},
+        "iters": rep.total_iters, "refinements": rep.restarts, "final_relres": rep.final_explicit_relres,
+        "converged": bool(rep.converged),
+        "ref_iters": REF_ITERS[args.config]["ir"],
+        "us_per_iter": ms_step * 1e3 / max(rep.total_iters, 1),
+        "gpu_launches": int(launches),
+        "kernels": kern,
+        "roofline": {"bound": "hbm", "kernel": names[top], "achieved": achieved, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic},
+    }
+    if not args.no_fp64:
+        cfg64 = mk.SolverConfig(m=50, rtol=1e-10, max_iters=100000)
+        solve64 = lambda: mk.gmres_restarted(A, None, b_dev, x0_dev, cfg64)  # noqa: E731
+        solve64()
+        ms64, reps64 = timed(solve64, 1)
+        out["fp64_gmres_s"] = ms64 / 1e3
+        out["fp64_iters"] = reps64[-1].total_iters
+        out["ir_speedup_vs_fp64"] = (ms64 / 1e3) / (ms_step / 1e3)
+    if not args.no_e2e:
+        bh = torch.ones(n, dtype=torch.float64).pin_memory()
+        xh = torch.zeros(n, dtype=torch.float64).pin_memory()
+        solve_e2e = lambda: mk.gmres_ir(A, bh, xh, icfg, A_low=A_low)  # noqa: E731
+        solve_e2e()
+        ms_e2e, reps_e = timed(solve_e2e, args.steps)
+        assert not reps_e[-1].x.is_cuda
+        out["e2e"] = {"value": ms_e2e / args.steps / 1e3, "unit": "s", "h2d_bytes_per_step": 2 * 8 * n,
+                      "d2h_bytes_per_step": 8 * n}
+    out["clocks"] = clk.summary()
+    if rank == 0 and world == 1 and not args.no_cpu:
+        s_it, it, dt = cpu_sample(args.config, "ir", 50)
+        full = REF_ITERS[args.config]["ir"] or rep.total_iters
+        out["cpu_baseline"] = {"value": s_it * full, "unit": "s", "cores": cpu_cores(), "kind": "port",
+                               "sample": "%d inner iterations (one refinement, %.1f s) of the same "
+                                         "GMRES-IR solve; s/iteration x reference count %d" % (it, dt, full)}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

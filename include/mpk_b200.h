@@ -190,7 +190,7 @@ typedef struct mpk_cycle_desc {
     void *ws;               /* mpk_reduce_ws_bytes(n, m + 2) */
     mpk_cycle_ctl *ctl;     /* device */
     int32_t nranks;         /* 1 (multi-rank cycles go through mpk_cycle_step_*) */
-    int32_t flags;          /* bit0: record per-kernel events for profiling */
+    int32_t flags;          /* bit0: per-kernel event timing; bit1: write the last basis column */
 } mpk_cycle_desc;
 
 int64_t mpk_cycle_hess_bytes(int32_t m, int32_t dtype);
@@ -237,6 +237,8 @@ int mpk_precond_apply(const mpk_precond *M, const void *v, void *out, void *stre
 /* classes: 0 SpMV+dot1, 1 update1+dot2, 2 update2+norm, 3 normalise, 4 precond,
  * 5 correction, 6 residual, 7 other */
 int mpk_prof_reset(void);
+/* number of kernels this library has enqueued so far (monotonic) */
+int64_t mpk_launch_count(void);
 /* totals[c] = summed milliseconds, counts[c] = launches, bytes[c] = algorithmic bytes */
 int mpk_prof_read(double *ms, int64_t *counts, double *bytes, int32_t nclasses);
 

@@ -21,6 +21,7 @@ using namespace mpk;
 namespace {
 
 thread_local std::string g_err;
+unsigned long long g_launches = 0;   // kernels enqueued by this library
 
 int fail(int code, const char *msg) {
     g_err = msg;
@@ -28,6 +29,7 @@ int fail(int code, const char *msg) {
 }
 
 int check_launch(const char *what) {
+    ++g_launches;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         g_err = std::string(what) + ": " + cudaGetErrorString(e);
@@ -443,11 +445,11 @@ int apply_precond_t(const mpk_precond *M, const T *v, T *out, const int32_t *don
                     auto k1 = k_poly_pair1<T, Op>;
                     int g = grid_for(k1, 0, op.n);
                     k1<<<g, kBlock, 0, s>>>(op, work, t, out, (T)tr, (T)m2, first ? 1 : 0, done);
-                    if (!last) {
-                        auto k2 = k_poly_pair2<T, Op>;
-                        k2<<<g, kBlock, 0, s>>>(op, work, t, wnext, (T)tr, (T)m2, done);
-                    }
-                    return check_launch("k_poly_pair");
+                    int rc1 = check_launch("k_poly_pair1");
+                    if (rc1 || last) return rc1;
+                    auto k2 = k_poly_pair2<T, Op>;
+                    k2<<<g, kBlock, 0, s>>>(op, work, t, wnext, (T)tr, (T)m2, done);
+                    return check_launch("k_poly_pair2");
                 });
                 i += 2;
             }
@@ -471,7 +473,9 @@ int apply_precond(const mpk_precond *M, const T *v, T *out, const int32_t *done,
     float *lo_in = (float *)M->work + 3 * n, *lo_out = lo_in + n;
     int g = grid_for(k_convert_gated<double, float>, 0, n);
     k_convert_gated<double, float><<<g, kBlock, 0, s>>>(n, (const double *)v, lo_in, done);
-    int rc = apply_precond_t<float>(M, lo_in, lo_out, done, s);
+    int rc = check_launch("k_convert_gated");
+    if (rc) return rc;
+    rc = apply_precond_t<float>(M, lo_in, lo_out, done, s);
     if (rc) return rc;
     k_convert_gated<float, double><<<g, kBlock, 0, s>>>(n, lo_out, (double *)out, done);
     return check_launch("k_convert_gated");
@@ -564,6 +568,11 @@ template <typename T> int run_cycle(const mpk_cycle_desc *d, cudaStream_t s) {
                               done, s);
             if (rc) return rc;
         }
+    }
+    if (d->flags & 2) {
+        int gf = grid_for(k_final_column<T>, 0, n);
+        k_final_column<T><<<gf, kBlock, 0, s>>>(n, wpp, sums + S_BETA, V, ld, ctl);
+        if ((rc = check_launch("k_final_column"))) return rc;
     }
     // epilogue: d = R \ g ; x_out = x0 + M(V_k d)
     k_lsq_solve<T><<<1, 32, (size_t)(m + 1) * sizeof(T), s>>>(H, ctl, u, 0);
@@ -817,6 +826,8 @@ int mpk_lsq_solve(int32_t dtype, int32_t m, int32_t k, void *hess, mpk_cycle_ctl
                                                              std::ldexp(1.0, -24), k);
     return check_launch("k_lsq_solve");
 }
+
+int64_t mpk_launch_count(void) { return (int64_t)g_launches; }
 
 int mpk_prof_reset(void) {
     prof_drain(true);

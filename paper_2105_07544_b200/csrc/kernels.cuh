@@ -398,6 +398,18 @@ __global__ void __launch_bounds__(kBlock) k_correct(int64_t n, const T *__restri
     }
 }
 
+// Diagnostics (collect_basis): write the last appended column
+// V[:, steps] = w'' / beta, which the fused cycle otherwise leaves to the
+// next step's P1 (gmres.py:198-199 returns basis.count columns).
+template <typename T>
+__global__ void k_final_column(int64_t n, const T *__restrict__ wpp, const T *betap, T *V, int64_t ld,
+                               const mpk_cycle_ctl *ctl) {
+    if (ctl->breakdown || ctl->steps <= 0) return;
+    T *col = V + (int64_t)ctl->steps * ld;
+    const T b = *betap;
+    for (int64_t r = gtid(); r < n; r += gstride()) col[r] = RN<T>::div(wpp[r], b);
+}
+
 // out = x0 + z  (the preconditioned correction, gmres.py:196); ctl gates it
 template <typename T>
 __global__ void k_add_gated(int64_t n, const T *__restrict__ x0, const T *__restrict__ z,

@@ -70,8 +70,21 @@ def to_host(t_):
     return t_.detach().cpu().numpy()
 
 
-def like_input(dev_tensor, was_host: bool):
-    return to_host(dev_tensor) if was_host else dev_tensor
+def like_input(dev_tensor, was_host):
+    """Return the result in the caller's kind: numpy for numpy input, a CPU
+    tensor for a CPU tensor input, the device tensor otherwise."""
+    if was_host is True:
+        return to_host(dev_tensor)
+    if was_host == "cpu_tensor":
+        return dev_tensor.detach().cpu()
+    return dev_tensor
+
+
+def host_kind(v):
+    """True (numpy), 'cpu_tensor', or False (CUDA tensor)."""
+    if not is_tensor(v):
+        return True
+    return False if v.is_cuda else "cpu_tensor"
 
 
 def empty(n, torch_dtype):
