@@ -190,7 +190,8 @@ typedef struct mpk_cycle_desc {
     void *ws;               /* mpk_reduce_ws_bytes(n, m + 2) */
     mpk_cycle_ctl *ctl;     /* device */
     int32_t nranks;         /* 1 (multi-rank cycles go through mpk_cycle_step_*) */
-    int32_t flags;          /* bit0: per-kernel event timing; bit1: write the last basis column */
+    int32_t flags;          /* bit0: per-kernel event timing; bit1: write the last basis column;
+                               bit2: force the multi-kernel cycle (no persistent kernel) */
 } mpk_cycle_desc;
 
 int64_t mpk_cycle_hess_bytes(int32_t m, int32_t dtype);

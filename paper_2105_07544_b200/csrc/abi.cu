@@ -14,7 +14,7 @@
 #include <utility>
 #include <vector>
 
-#include "kernels.cuh"
+#include "fused.cuh"
 
 using namespace mpk;
 
@@ -183,6 +183,8 @@ StencilConsts stencil_consts(const mpk_matrix *A) {
     k.nglob = (A->preset == MPK_LAPLACE3D) ? (int64_t)A->nx * A->nx * A->nx : (int64_t)A->nx * A->nx;
     volatile double h = 1.0 / (nx + 1.0);   // stencils.py:87
     k.h = h;
+    k.dnx.init((uint32_t)A->nx);
+    k.dnxy.init((uint32_t)A->nx * (uint32_t)A->nx);
     switch (A->preset) {
     case MPK_LAPLACE2D: {
         const double c[5] = {-1.0, -1.0, 4.0, -1.0, -1.0};
@@ -501,6 +503,56 @@ template <typename T> int run_cycle(const mpk_cycle_desc *d, cudaStream_t s) {
     const double u = (sizeof(T) == 8) ? std::ldexp(1.0, -53) : std::ldexp(1.0, -24);
     const double tf = (d->rule == MPK_RULE_U) ? u : (double)n * u;   // kernels.py:122
     int rc;
+
+    if (!precond && m + 1 <= kFMaxCols && d->nranks <= 1 && !(d->flags & 4)) {
+        // persistent cooperative cycle: one launch for the whole cycle
+        return with_op<T>(d->A, [&](auto op) -> int {
+            using Op = decltype(op);
+            auto kern = k_cycle_fused<T, Op>;
+            const size_t smem = sizeof(T) * ((size_t)(m + 1) * m + 2 * m + (m + 1) + 2 * kFSlots + 8 +
+                                             2 * kFB * Vec16<T>::R + kFW);
+            static bool attr_set = false;
+            if (!attr_set) {
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+                attr_set = true;
+            }
+            int per_sm = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFB, smem);
+            if (per_sm < 1) return fail(MPK_ELAUNCH, "fused cycle kernel does not fit on an SM");
+            int grid = sm_count_cached() * (per_sm > 1 ? 1 : per_sm);
+            if (grid > kFMaxCtas) grid = kFMaxCtas;
+            FusedArgs<T> fa;
+            fa.n = n;
+            fa.ld = ld;
+            fa.m = m;
+            fa.cap = cap;
+            fa.V = V;
+            fa.r0 = (const T *)d->r0;
+            fa.rnorm2 = (const T *)d->rnorm2;
+            fa.x0 = (const T *)d->x0;
+            fa.x_out = (T *)d->x_out;
+            fa.w = w;
+            fa.wp = wp;
+            fa.wpp = wpp;
+            fa.part = (T *)ws.partials;
+            fa.bar = ws.counters + 8;
+            fa.H = H;
+            fa.ctl = ctl;
+            fa.tf = tf;
+            fa.exit_tol = d->exit_tol;
+            fa.norm_scale = d->norm_scale;
+            fa.u = u;
+            fa.final_col = (d->flags & 2) ? 1 : 0;
+            void *args[] = {(void *)&op, (void *)&fa};
+            ProfScope ps(7, 0.0, s);
+            cudaError_t e = cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(kFB), args, smem, s);
+            if (e != cudaSuccess) {
+                g_err = std::string("k_cycle_fused: ") + cudaGetErrorString(e);
+                return MPK_ELAUNCH;
+            }
+            return check_launch("k_cycle_fused");
+        });
+    }
 
     k_cycle_begin<T><<<1, 32, 0, s>>>((const T *)d->rnorm2, sums, H, ctl, d->norm_scale);
     if ((rc = check_launch("k_cycle_begin"))) return rc;

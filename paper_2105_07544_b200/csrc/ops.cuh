@@ -31,6 +31,21 @@ template <typename T> struct CsrOp {
     static constexpr bool kStencil = false;
 };
 
+// Division by a grid-invariant divisor (nx, nx^2) without the integer
+// divider: q = (umulhi(x, mul) + x) >> shift, exact for x < 2^31.
+struct FastDiv {
+    uint32_t d, mul, shift;
+    __host__ void init(uint32_t dv) {
+        d = dv;
+        shift = 0;
+        while ((1ull << shift) < dv) ++shift;
+        mul = (uint32_t)(((1ull << 32) * ((1ull << shift) - dv)) / dv + 1);
+    }
+    __device__ __forceinline__ uint32_t div(uint32_t x) const {
+        return (__umulhi(x, mul) + x) >> shift;
+    }
+};
+
 // Host-computed constants of a stencil preset (double, reference formulas).
 struct StencilConsts {
     int preset;
@@ -40,6 +55,7 @@ struct StencilConsts {
     double c[9];         // constant coefficients (displacement order)
     double h, hh;        // h = 1/(nx+1), hh = 0.5*h      (BentPipe)
     double cc2, ncc2;    // c*2.0 and (-c)*2.0            (BentPipe)
+    FastDiv dnx, dnxy;   // division by nx and nx^2 (n < 2^31)
 };
 
 template <typename T> struct StencilOp {
@@ -48,12 +64,15 @@ template <typename T> struct StencilOp {
     T cT[9];
 
     template <class X> __device__ __forceinline__ T row(int64_t r, X x) const {
-        const int64_t g = k.row0 + r;
+        const uint32_t g = (uint32_t)(k.row0 + r);
         const int nx = k.nx;
         T acc = T(0);
+        const uint32_t q1 = k.dnx.div(g);
+        const int ix = (int)(g - q1 * (uint32_t)nx);
         if (k.preset == MPK_LAPLACE3D) {
             const int64_t nxy = (int64_t)nx * nx;
-            const int ix = (int)(g % nx), iy = (int)((g / nx) % nx), iz = (int)(g / nxy);
+            const uint32_t iz_ = k.dnxy.div(g);
+            const int iy = (int)(q1 - iz_ * (uint32_t)nx), iz = (int)iz_;
             if (iz > 0) acc = RN<T>::add(acc, RN<T>::mul(cT[0], x(r - nxy)));
             if (iy > 0) acc = RN<T>::add(acc, RN<T>::mul(cT[1], x(r - nx)));
             if (ix > 0) acc = RN<T>::add(acc, RN<T>::mul(cT[2], x(r - 1)));
@@ -63,7 +82,7 @@ template <typename T> struct StencilOp {
             if (iz < nx - 1) acc = RN<T>::add(acc, RN<T>::mul(cT[6], x(r + nxy)));
             return acc;
         }
-        const int ix = (int)(g % nx), iy = (int)(g / nx);
+        const int iy = (int)q1;
         if (k.preset == MPK_STRETCHED2D) {
             const bool W = ix > 0, E = ix < nx - 1, S = iy > 0, N = iy < nx - 1;
             if (W && S) acc = RN<T>::add(acc, RN<T>::mul(cT[0], x(r - nx - 1)));
@@ -109,6 +128,12 @@ template <typename T> struct XScaled {
     const T *__restrict__ p;
     T d;
     __device__ __forceinline__ T operator()(int64_t c) const { return RN<T>::div(p[c], d); }
+};
+// same, reading through L2 (data written by other CTAs of a persistent kernel)
+template <typename T> struct XScaledCG {
+    const T *p;
+    T d;
+    __device__ __forceinline__ T operator()(int64_t c) const { return RN<T>::div(__ldcg(p + c), d); }
 };
 
 }  // namespace mpk

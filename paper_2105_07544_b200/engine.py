@@ -49,7 +49,9 @@ class CycleWorkspace:
         self.ld = D.ld_for(n)
         td = prec.torch_dtype
         dev = D.device()
-        self.V = t.empty((self.m + 1) * self.ld, dtype=td, device=dev)
+        # zero-initialised: rows [n, ld) of every column stay zero (the fused
+        # kernel's 16-byte row groups and chunk tails read them)
+        self.V = t.zeros((self.m + 1) * self.ld, dtype=td, device=dev)
         self.work = t.zeros(4 * self.ld, dtype=td, device=dev)
         self.hess = t.zeros(int(lib.mpk_cycle_hess_bytes(self.m, prec.code)), dtype=t.uint8, device=dev)
         self.ws = D.ReduceWorkspace()
