@@ -509,11 +509,11 @@ template <typename T> int run_cycle(const mpk_cycle_desc *d, cudaStream_t s) {
         return with_op<T>(d->A, [&](auto op) -> int {
             using Op = decltype(op);
             auto kern = k_cycle_fused<T, Op>;
-            const size_t smem = sizeof(T) * ((size_t)(m + 1) * m + 2 * m + (m + 1) + 2 * kFSlots + 8 +
-                                             2 * kFB * Vec16<T>::R + kFW);
+            const size_t smem = (size_t)kStages * kStageBytes + 64 +
+                                sizeof(T) * ((size_t)(m + 1) * m + 2 * m + (m + 1) + 2 * kFSlots + kFB + kMaxTR + kFW);
             static bool attr_set = false;
             if (!attr_set) {
-                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
                 attr_set = true;
             }
             int per_sm = 0;

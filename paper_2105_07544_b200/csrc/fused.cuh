@@ -11,19 +11,25 @@
 // extra broadcast barrier, no kernel launches inside the cycle:
 //
 //   A  v_k = w''/beta (own rows -> V[:,k]), w = A v_k (neighbours read w''
-//      through L2), ||w||^2, c1 = V[:,0..k]^T w            -> barrier, reduce
-//   B  w' = w - V c1 (row-wise), c2 = V^T w' (column-wise; the chunk of V is
-//      re-read from L1/L2, HBM sees it once)               -> barrier, reduce
+//      through L2), ||w||^2; then c1 = V[:,0..k]^T w       -> barrier, reduce
+//   B  w' = w - V c1 (row-wise), c2 = V^T w' (column-wise) -> barrier, reduce
 //   C  w'' = w' - V c2, ||w''||^2                          -> barrier, reduce
 //      beta, append test (kernels.py:122), Givens (kernels.py:183-196), exit
 //
+// Streaming: the basis and the work vector of a phase are moved HBM ->
+// shared memory by the TMA engine (cp.async.bulk, one bulk copy per column
+// of a TR-row tile, completion on an mbarrier) through a 4-stage, 32 KB/stage
+// ring, so bytes in flight are bounded by shared memory, not registers.  Each
+// tile is consumed from shared memory: row-wise combinations (thread per row,
+// P = 512/TR column parts summed in fixed order) and column-wise dots (one
+// warp per column).  HBM sees every basis column exactly once per phase.
+//
 // Epilogue: each CTA back-substitutes R d = g (kernels.py:202-216) from its
 // shared-memory copy of R and forms x_out = x0 + V_k d for its own rows.
-// Dot products: row-wise -> thread accumulators; column-wise -> one warp per
-// column (16 warps x 4 columns), lanes striding the chunk's rows.
 #pragma once
 
 #include "kernels.cuh"
+#include "tma.cuh"
 
 namespace mpk {
 
@@ -34,8 +40,9 @@ constexpr int kFQ = kFMaxCols / kFW;    // columns owned per warp
 constexpr int kFExtra = kFMaxCols;      // partial slot of the extra scalar
 constexpr int kFSlots = kFMaxCols + 1;
 constexpr int kFMaxCtas = 320;          // per-slot stride of the partials
-constexpr int kCombineBatch = 8;        // 16-byte column loads in flight per row group
-constexpr int kDotBatch = 8;            // 16-byte loads in flight per lane per column
+constexpr int kStages = 4;              // TMA ring depth
+constexpr int kStageBytes = 32 * 1024;  // bytes per ring stage
+constexpr int kMaxTR = 2048;            // rows per tile (upper bound)
 
 template <typename T> struct FusedArgs {
     int64_t n, ld;
@@ -120,99 +127,103 @@ __device__ __forceinline__ void write_partials(T (&acc)[kFQ], int ncols, T extra
     }
 }
 
-// 16-byte row groups: RPT consecutive rows per thread (4 fp32 / 2 fp64),
-// loaded from the column-major basis with one 16-byte load per column.
-template <typename T> struct Vec16;
-template <> struct Vec16<float> {
-    using type = float4;
-    static constexpr int R = 4;
-    static __device__ __forceinline__ float get(const float4 &v, int i) {
-        return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
-    }
-};
-template <> struct Vec16<double> {
-    using type = double2;
-    static constexpr int R = 2;
-    static __device__ __forceinline__ double get(const double2 &v, int i) { return i == 0 ? v.x : v.y; }
-};
 
-// s[e] = sum_{c < nc} V[c, r + e] * coef[c], e < RPT; 16 columns in flight.
-template <typename T>
-__device__ __forceinline__ void group_combine(const T *V, int64_t ld, int64_t r, int nc, const T *coef,
-                                              T (&s)[Vec16<T>::R]) {
-    using VT = typename Vec16<T>::type;
-    constexpr int R = Vec16<T>::R;
-#pragma unroll
-    for (int e = 0; e < R; ++e) s[e] = T(0);
-    constexpr int G = kCombineBatch;
-    for (int c = 0; c < nc; c += G) {
-        VT v[G];
-#pragma unroll
-        for (int q = 0; q < G; ++q)
-            if (c + q < nc) v[q] = *reinterpret_cast<const VT *>(V + (int64_t)(c + q) * ld + r);
-#pragma unroll
-        for (int q = 0; q < G; ++q)
-            if (c + q < nc) {
-                const T cf = coef[c + q];
-#pragma unroll
-                for (int e = 0; e < R; ++e) s[e] += Vec16<T>::get(v[q], e) * cf;
-            }
-    }
+// Rows per tile for `ncols` streamed columns: the largest power of two with
+// ncols*TR*sizeof(T) <= kStageBytes, clamped to [32, kMaxTR].
+template <typename T> __device__ __forceinline__ int tile_rows(int ncols) {
+    int tr = kMaxTR;
+    while (tr > 32 && (int64_t)ncols * tr * (int64_t)sizeof(T) > kStageBytes) tr >>= 1;
+    return tr;
 }
 
-// Row-wise s = sum_c V[c, r] * coef[c] for c < nc (coef in shared memory);
-// loads issued in groups of 16 independent columns.
+// Shared-memory ring of bulk-copy stages; `gt` counts tiles over the whole
+// kernel (identical in every thread) so stage = gt % S, parity = (gt / S) & 1.
+struct Ring {
+    unsigned char *base;
+    uint64_t *full;
+    uint32_t gt;
+};
+
 template <typename T>
-__device__ __forceinline__ T row_combine(const T *V, int64_t ld, int64_t r, int nc, const T *coef) {
+__device__ __forceinline__ void ring_issue(Ring &R, uint32_t g, int TR, const T *V, int64_t ld, int nv, const T *vec,
+                                           int64_t t0) {
+    const int slot = (int)(g % kStages);
+    T *stage = reinterpret_cast<T *>(R.base + (size_t)slot * kStageBytes);
+    int64_t rows = ld - t0;
+    if (rows > TR) rows = TR;
+    const uint32_t bytes = (uint32_t)(rows * (int64_t)sizeof(T));
+    mbar_arrive_expect_tx(&R.full[slot], bytes * (uint32_t)(nv + (vec ? 1 : 0)));
+    for (int c = 0; c < nv; ++c) bulk_g2s(stage + (int64_t)c * TR, V + (int64_t)c * ld + t0, bytes, &R.full[slot]);
+    if (vec) bulk_g2s(stage + (int64_t)nv * TR, vec + t0, bytes, &R.full[slot]);
+}
+
+// Stream the CTA's rows [rb, re) in TR-row tiles of (V[:, 0..nv) | vec) and
+// call consume(stage, t0, rows) on each; all threads participate.
+template <typename T, class F>
+__device__ __forceinline__ void stream_phase(Ring &R, int64_t rb, int64_t re, int TR, const T *V, int64_t ld, int nv,
+                                             const T *vec, F &&consume) {
+    const int ntiles = (re > rb) ? (int)((re - rb + TR - 1) / TR) : 0;
+    fence_proxy_async_all();   // generic writes (own rows of V, w) before TMA reads
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int pre = ntiles < kStages ? ntiles : kStages;
+        for (int i = 0; i < pre; ++i) ring_issue<T>(R, R.gt + i, TR, V, ld, nv, vec, rb + (int64_t)i * TR);
+    }
+    for (int i = 0; i < ntiles; ++i) {
+        const uint32_t g = R.gt + i;
+        const int slot = (int)(g % kStages);
+        mbar_wait(&R.full[slot], (g / kStages) & 1u);
+        const int64_t t0 = rb + (int64_t)i * TR;
+        const int rows = (int)((re - t0) < TR ? (re - t0) : TR);
+        consume(reinterpret_cast<const T *>(R.base + (size_t)slot * kStageBytes), t0, rows);
+        fence_proxy_async_all();   // generic reads of the stage before it is refilled
+        __syncthreads();
+        if (threadIdx.x == 0 && i + kStages < ntiles)
+            ring_issue<T>(R, g + kStages, TR, V, ld, nv, vec, rb + (int64_t)(i + kStages) * TR);
+    }
+    R.gt += ntiles;
+}
+
+// Row-wise s[rr] = sum_{c < nc} stage[c][rr] * coef[c] for rr < rows; calls
+// fin(rr, s).  TR >= kFB: each thread owns rows tid, tid+kFB, ...; TR < kFB:
+// P = kFB/TR threads share a row (columns strided by P), partial sums
+// combined in part order through `spart` (P*TR elements).
+template <typename T, class Fin>
+__device__ __forceinline__ void tile_rowcombine(const T *stage, int TR, int rows, int nc, const T *coef, T *spart,
+                                                Fin &&fin) {
+    const int tid = threadIdx.x;
+    if (TR >= kFB) {
+        for (int rr = tid; rr < rows; rr += kFB) {
+            T s = T(0);
+            for (int c = 0; c < nc; ++c) s += stage[(int64_t)c * TR + rr] * coef[c];
+            fin(rr, s);
+        }
+        return;
+    }
+    const int P = kFB / TR, rr = tid % TR, p = tid / TR;
     T s = T(0);
-    int c = 0;
-    for (; c + 16 <= nc; c += 16) {
-        T v[16];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) v[q] = V[(int64_t)(c + q) * ld + r];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) s += v[q] * coef[c + q];
+    for (int c = p; c < nc; c += P) s += stage[(int64_t)c * TR + rr] * coef[c];
+    spart[p * TR + rr] = s;
+    __syncthreads();
+    if (p == 0 && rr < rows) {
+        T t = spart[rr];
+        for (int q = 1; q < P; ++q) t += spart[q * TR + rr];
+        fin(rr, t);
     }
-    if (c < nc) {
-        T v[16];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) v[q] = (c + q < nc) ? V[(int64_t)(c + q) * ld + r] : T(0);
-#pragma unroll
-        for (int q = 0; q < 16; ++q)
-            if (c + q < nc) s += v[q] * coef[c + q];
-    }
-    return s;
 }
 
-// Column-wise acc[q] += sum_{rows of chunk} V[c, row] * x[row] for the
-// warp's columns c = warp + kFW*q < nc.  The chunk is kFB*RPT rows; lane l
-// reads 16-byte groups l, l+32, ... of the column; x (and, for column
-// own_c, the column itself) come from shared memory as 16-byte groups.
+// Column-wise acc[q] += sum_{rr < rows} stage[c][rr] * x[rr] for the warp's
+// columns c = warp + kFW*q < nc.
 template <typename T>
-__device__ __forceinline__ void col_dots(const T *V, int64_t ld, int64_t c0, int nc, const T *x,
-                                         int own_c, const T *own, T (&acc)[kFQ]) {
-    using VT = typename Vec16<T>::type;
-    constexpr int R = Vec16<T>::R;
+__device__ __forceinline__ void tile_coldots(const T *stage, int TR, int rows, int nc, const T *x, T (&acc)[kFQ]) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const VT *xv = reinterpret_cast<const VT *>(x);
 #pragma unroll
     for (int q = 0; q < kFQ; ++q) {
         const int c = warp + kFW * q;
         if (c < nc) {
-            const VT *col = reinterpret_cast<const VT *>(c == own_c ? own : V + (int64_t)c * ld + c0);
+            const T *col = stage + (int64_t)c * TR;
             T s = T(0);
-#pragma unroll
-            for (int h = 0; h < kFB / 32; h += kDotBatch) {
-                VT v[kDotBatch];
-#pragma unroll
-                for (int i = 0; i < kDotBatch; ++i) v[i] = col[lane + 32 * (h + i)];
-#pragma unroll
-                for (int i = 0; i < kDotBatch; ++i) {
-                    const VT xx = xv[lane + 32 * (h + i)];
-#pragma unroll
-                    for (int e = 0; e < R; ++e) s += Vec16<T>::get(v[i], e) * Vec16<T>::get(xx, e);
-                }
-            }
+            for (int rr = lane; rr < rows; rr += 32) s += col[rr] * x[rr];
             acc[q] += s;
         }
     }
@@ -220,19 +231,21 @@ __device__ __forceinline__ void col_dots(const T *V, int64_t ld, int64_t c0, int
 
 template <typename T, class Op>
 __global__ void __launch_bounds__(kFB, 1) k_cycle_fused(Op A, FusedArgs<T> a) {
-    extern __shared__ unsigned char dsm_raw[];
+    extern __shared__ __align__(128) unsigned char dsm_raw[];
     const int m = a.m, ldr = m + 1;
-    T *sR = reinterpret_cast<T *>(dsm_raw);   // (m+1) x m rotated columns
+    Ring R;
+    R.base = dsm_raw;                                                    // kStages * kStageBytes
+    R.full = reinterpret_cast<uint64_t *>(dsm_raw + kStages * kStageBytes);
+    R.gt = 0;
+    T *sR = reinterpret_cast<T *>(dsm_raw + kStages * kStageBytes + 64);  // (m+1) x m rotated columns
     T *scs = sR + (int64_t)ldr * m;
     T *ssn = scs + m;
     T *sg = ssn + m;                           // m + 1
     T *sc1 = sg + (m + 1);                     // kFSlots
     T *sc2 = sc1 + kFSlots;                    // kFSlots
-    constexpr int R = Vec16<T>::R;
-    constexpr int CH = kFB * R;                // rows per chunk
-    T *sx = reinterpret_cast<T *>(reinterpret_cast<uintptr_t>(sc2 + kFSlots + 1) & ~uintptr_t(15)) + 4;
-    T *sv = sx + CH;                           // chunk of v_k (16-byte aligned)
-    T *sred = sv + CH;                         // kFW
+    T *spart = sc2 + kFSlots;                  // kFB
+    T *sx = spart + kFB;                       // kMaxTR (w' of the tile)
+    T *sred = sx + kMaxTR;                     // kFW
     __shared__ T s_gamma, s_beta, s_bn2;
     __shared__ int s_done, s_steps, s_break, s_app;
     __shared__ double s_scale;
@@ -247,6 +260,8 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_fused(Op A, FusedArgs<T> a) {
     const bool lead = (blockIdx.x == 0);
 
     if (tid == 0) {
+        for (int i = 0; i < kStages; ++i) mbar_init(&R.full[i], 1);
+        fence_mbar_init();
         const T gamma = RN<T>::sqrt_(__ldcg(a.rnorm2));
         s_gamma = gamma;
         double scale = a.norm_scale > 0.0 ? a.norm_scale : (double)gamma;
@@ -273,73 +288,52 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_fused(Op A, FusedArgs<T> a) {
         const T *src = (k == 0) ? a.r0 : a.wpp;
         const T dv = (k == 0) ? s_gamma : s_beta;
         T *vk = a.V + (int64_t)k * a.ld;
+        const int TR = tile_rows<T>(nc + 1);
         T acc[kFQ];
-        // ---------------- phase A: normalise, SpMV, ||w||^2, V^T w
+        // ---------------- phase A: v_k = src/dv, w = A v_k, ||w||^2 ; c1 = V^T w
+        T an = T(0);
+        for (int64_t r = rb + tid; r < re; r += kFB) {
+            vk[r] = RN<T>::div(__ldcg(src + r), dv);
+            const T wr = A.row(r, XScaledCG<T>{src, dv});
+            a.w[r] = wr;
+            an += wr * wr;
+        }
 #pragma unroll
         for (int q = 0; q < kFQ; ++q) acc[q] = T(0);
-        T an = T(0);
-        for (int64_t c0 = rb; c0 < re; c0 += CH) {
-#pragma unroll
-            for (int e = 0; e < R; ++e) {
-                const int lr = tid * R + e;
-                const int64_t r = c0 + lr;
-                T own = T(0), wr = T(0);
-                if (r < re) {
-                    own = RN<T>::div(__ldcg(src + r), dv);
-                    vk[r] = own;
-                    wr = A.row(r, XScaledCG<T>{src, dv});
-                    a.w[r] = wr;
-                    an += wr * wr;
-                }
-                sv[lr] = own;
-                sx[lr] = wr;
-            }
-            __syncthreads();
-            col_dots<T>(a.V, a.ld, c0, nc, sx, k, sv, acc);
-            __syncthreads();
-        }
+        stream_phase<T>(R, rb, re, TR, a.V, a.ld, nc, a.w, [&](const T *st, int64_t, int rows) {
+            tile_coldots<T>(st, TR, rows, nc, st + (int64_t)nc * TR, acc);
+        });
         write_partials<T>(acc, nc, an, sred, partA);
         grid_sync(a.bar, nb);
         cross_reduce<T>(partA, nb, nc, nc + 1, sc1);   // sc1[0..k], sc1[nc] = ||w||^2
         __syncthreads();
-        // ---------------- phase B: w' = w - V c1 ; V^T w'
+        // ---------------- phase B: w' = w - V c1 ; c2 = V^T w'
 #pragma unroll
         for (int q = 0; q < kFQ; ++q) acc[q] = T(0);
-        for (int64_t c0 = rb; c0 < re; c0 += CH) {
-            const int64_t r = c0 + tid * R;
-            T sl[R];
-            if (r < re) group_combine<T>(a.V, a.ld, r, nc, sc1, sl);
-#pragma unroll
-            for (int e = 0; e < R; ++e) {
-                T wr = T(0);
-                if (r + e < re) {
-                    wr = RN<T>::sub(a.w[r + e], sl[e]);
-                    a.wp[r + e] = wr;
-                }
-                sx[tid * R + e] = wr;
-            }
+        stream_phase<T>(R, rb, re, TR, a.V, a.ld, nc, a.w, [&](const T *st, int64_t t0, int rows) {
+            const T *wv = st + (int64_t)nc * TR;
+            tile_rowcombine<T>(st, TR, rows, nc, sc1, spart, [&](int rr, T s) {
+                const T wr = RN<T>::sub(wv[rr], s);
+                a.wp[t0 + rr] = wr;
+                sx[rr] = wr;
+            });
             __syncthreads();
-            col_dots<T>(a.V, a.ld, c0, nc, sx, -1, sv, acc);
-            __syncthreads();
-        }
+            tile_coldots<T>(st, TR, rows, nc, sx, acc);
+        });
         write_partials<T>(acc, nc, T(0), sred, partB);
         grid_sync(a.bar, nb);
         cross_reduce<T>(partB, nb, nc, nc, sc2);
         __syncthreads();
         // ---------------- phase C: w'' = w' - V c2 ; ||w''||^2
         T bn = T(0);
-        for (int64_t r = rb + tid * R; r < re; r += CH) {
-            T sl[R];
-            group_combine<T>(a.V, a.ld, r, nc, sc2, sl);
-#pragma unroll
-            for (int e = 0; e < R; ++e) {
-                if (r + e < re) {
-                    const T wr = RN<T>::sub(a.wp[r + e], sl[e]);
-                    a.wpp[r + e] = wr;
-                    bn += wr * wr;
-                }
-            }
-        }
+        stream_phase<T>(R, rb, re, TR, a.V, a.ld, nc, a.wp, [&](const T *st, int64_t t0, int rows) {
+            const T *wv = st + (int64_t)nc * TR;
+            tile_rowcombine<T>(st, TR, rows, nc, sc2, spart, [&](int rr, T s) {
+                const T wr = RN<T>::sub(wv[rr], s);
+                a.wpp[t0 + rr] = wr;
+                bn += wr * wr;
+            });
+        });
         {
             T dummy[kFQ];
 #pragma unroll
@@ -446,17 +440,25 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_fused(Op A, FusedArgs<T> a) {
     }
     __syncthreads();
     if (k > 0 && s_app) return;   // TriangularBreakdownError: x_out untouched
+    if (lead) {
+        for (int i = tid; i < k; i += kFB) a.H.d[i] = sd[i];
+        for (int i = tid; i < k * ldr; i += kFB) a.H.h[i] = sR[i];
+        for (int i = tid; i <= k; i += kFB) a.H.g[i] = sg[i];
+    }
     if (a.final_col && k > 0 && !s_break) {
         T *vn = a.V + (int64_t)k * a.ld;
         for (int64_t r = rb + tid; r < re; r += kFB) vn[r] = RN<T>::div(a.wpp[r], s_beta);
     }
-    for (int64_t r = rb + tid * R; r < re; r += CH) {
-        T sl[R];
-        if (k > 0) group_combine<T>(a.V, a.ld, r, k, sd, sl);
-#pragma unroll
-        for (int e = 0; e < R; ++e)
-            if (r + e < re) a.x_out[r + e] = (k == 0) ? a.x0[r + e] : RN<T>::add(a.x0[r + e], sl[e]);
+    if (k == 0) {
+        for (int64_t r = rb + tid; r < re; r += kFB) a.x_out[r] = a.x0[r];
+        return;
     }
+    const int TRe = tile_rows<T>(k);
+    stream_phase<T>(R, rb, re, TRe, a.V, a.ld, k, (const T *)nullptr, [&](const T *st, int64_t t0, int rows) {
+        tile_rowcombine<T>(st, TRe, rows, k, sd, spart, [&](int rr, T s) {
+            a.x_out[t0 + rr] = RN<T>::add(a.x0[t0 + rr], s);
+        });
+    });
 }
 
 }  // namespace mpk
