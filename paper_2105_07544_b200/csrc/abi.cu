@@ -3,6 +3,8 @@
 // runtime of one restarted-GMRES cycle: it enqueues every kernel of the
 // cycle on the caller's stream without synchronising; early exits are
 // device-side (ctl->done), so the host reads back once per cycle.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -486,6 +488,29 @@ int apply_precond(const mpk_precond *M, const T *v, T *out, const int32_t *done,
 // ---------------------------------------------------------------------------
 // one GMRES cycle
 // ---------------------------------------------------------------------------
+// 2-D tensor map of a column-major basis V (ld rows x ncols columns) with
+// TR x kCB boxes; out-of-range rows/columns read as zero.
+int encode_basis_map(CUtensorMap *map, const void *V, int64_t ld, int ncols, int sv, int TR) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    if (!enc) {
+        cudaDriverEntryPointQueryResult q;
+        void *fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+            return fail(MPK_ELAUNCH, "cuTensorMapEncodeTiled unavailable");
+        enc = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    }
+    cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)ncols};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * sv};
+    cuuint32_t box[2] = {(cuuint32_t)TR, (cuuint32_t)kCB};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, sv == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                     const_cast<void *>(V), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(MPK_ELAUNCH, "cuTensorMapEncodeTiled failed");
+    return MPK_OK;
+}
+
 template <typename T> int run_cycle(const mpk_cycle_desc *d, cudaStream_t s) {
     const int64_t n = d->n, ld = d->ld;
     const int m = d->m;
@@ -509,12 +534,20 @@ template <typename T> int run_cycle(const mpk_cycle_desc *d, cudaStream_t s) {
         return with_op<T>(d->A, [&](auto op) -> int {
             using Op = decltype(op);
             auto kern = k_cycle_fused<T, Op>;
-            const size_t smem = (size_t)kStages * kStageBytes + 64 +
-                                sizeof(T) * ((size_t)(m + 1) * m + 2 * m + (m + 1) + 2 * kFSlots + kFB + kMaxTR + kFW);
-            static bool attr_set = false;
-            if (!attr_set) {
-                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-                attr_set = true;
+            const size_t smem = (size_t)kRingBytes + 8 * kMaxStages +
+                                sizeof(T) * ((size_t)(m + 1) * m + 2 * m + (m + 1) + 2 * kFSlots + kFB +
+                                             TileRows<T>::value + kFW);
+            CUtensorMap tmap;
+            int erc = encode_basis_map(&tmap, V, ld, m + 1, (int)sizeof(T), TileRows<T>::value);
+            if (erc) return erc;
+            static size_t attr_set = 0;
+            if (smem > attr_set) {
+                cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                if (ea != cudaSuccess) {
+                    g_err = std::string("k_cycle_fused smem attribute: ") + cudaGetErrorString(ea);
+                    return MPK_ELAUNCH;
+                }
+                attr_set = smem;
             }
             int per_sm = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFB, smem);
@@ -543,7 +576,7 @@ template <typename T> int run_cycle(const mpk_cycle_desc *d, cudaStream_t s) {
             fa.norm_scale = d->norm_scale;
             fa.u = u;
             fa.final_col = (d->flags & 2) ? 1 : 0;
-            void *args[] = {(void *)&op, (void *)&fa};
+            void *args[] = {(void *)&op, (void *)&fa, (void *)&tmap};
             ProfScope ps(7, 0.0, s);
             cudaError_t e = cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(kFB), args, smem, s);
             if (e != cudaSuccess) {

@@ -40,9 +40,11 @@ constexpr int kFQ = kFMaxCols / kFW;    // columns owned per warp
 constexpr int kFExtra = kFMaxCols;      // partial slot of the extra scalar
 constexpr int kFSlots = kFMaxCols + 1;
 constexpr int kFMaxCtas = 320;          // per-slot stride of the partials
-constexpr int kStages = 4;              // TMA ring depth
-constexpr int kStageBytes = 32 * 1024;  // bytes per ring stage
-constexpr int kMaxTR = 2048;            // rows per tile (upper bound)
+constexpr int kMaxStages = 8;           // TMA ring depth (upper bound)
+constexpr int kRingBytes = 176 * 1024;  // shared memory of the ring
+constexpr int kCB = 16;                 // basis columns per tensor-map box
+constexpr int kMaxTR = 256;             // rows per tile (fp32; fp64 uses 128)
+template <typename T> struct TileRows { static constexpr int value = 1024 / sizeof(T); };
 
 template <typename T> struct FusedArgs {
     int64_t n, ld;
@@ -128,60 +130,76 @@ __device__ __forceinline__ void write_partials(T (&acc)[kFQ], int ncols, T extra
 }
 
 
-// Rows per tile for `ncols` streamed columns: the largest power of two with
-// ncols*TR*sizeof(T) <= kStageBytes, clamped to [32, kMaxTR].
-template <typename T> __device__ __forceinline__ int tile_rows(int ncols) {
-    int tr = kMaxTR;
-    while (tr > 32 && (int64_t)ncols * tr * (int64_t)sizeof(T) > kStageBytes) tr >>= 1;
-    return tr;
-}
-
-// Shared-memory ring of bulk-copy stages; `gt` counts tiles over the whole
-// kernel (identical in every thread) so stage = gt % S, parity = (gt / S) & 1.
+// Shared-memory ring of TMA stages.  A stage holds a TR-row tile of the
+// basis columns [0, nv) (ceil(nv/kCB) tensor-map boxes of TR x kCB, column
+// c at offset c*TR) followed by the tile of one work vector (1-D bulk copy).
+// The number of stages adapts to the tile size; `phase` holds the next wait
+// parity of each mbarrier (identical in every thread).
 struct Ring {
     unsigned char *base;
     uint64_t *full;
-    uint32_t gt;
+    uint32_t phase;
 };
 
 template <typename T>
-__device__ __forceinline__ void ring_issue(Ring &R, uint32_t g, int TR, const T *V, int64_t ld, int nv, const T *vec,
-                                           int64_t t0) {
-    const int slot = (int)(g % kStages);
-    T *stage = reinterpret_cast<T *>(R.base + (size_t)slot * kStageBytes);
-    int64_t rows = ld - t0;
-    if (rows > TR) rows = TR;
-    const uint32_t bytes = (uint32_t)(rows * (int64_t)sizeof(T));
-    mbar_arrive_expect_tx(&R.full[slot], bytes * (uint32_t)(nv + (vec ? 1 : 0)));
-    for (int c = 0; c < nv; ++c) bulk_g2s(stage + (int64_t)c * TR, V + (int64_t)c * ld + t0, bytes, &R.full[slot]);
-    if (vec) bulk_g2s(stage + (int64_t)nv * TR, vec + t0, bytes, &R.full[slot]);
+__device__ __forceinline__ void ring_issue(Ring &R, int slot, size_t sbytes, int TR, const CUtensorMap *tmV, int nv,
+                                           const T *vec, int64_t t0) {
+    T *stage = reinterpret_cast<T *>(R.base + (size_t)slot * sbytes);
+    const int nbox = (nv + kCB - 1) / kCB;
+    const uint32_t boxb = (uint32_t)(TR * kCB * sizeof(T));
+    const uint32_t vb = (uint32_t)(TR * sizeof(T));
+    mbar_arrive_expect_tx(&R.full[slot], boxb * nbox + (vec ? vb : 0u));
+    for (int b = 0; b < nbox; ++b)
+        tma_load_2d(stage + (int64_t)b * kCB * TR, tmV, (int)t0, b * kCB, &R.full[slot]);
+    if (vec) bulk_g2s(stage + (int64_t)nbox * kCB * TR, vec + t0, vb, &R.full[slot]);
 }
 
 // Stream the CTA's rows [rb, re) in TR-row tiles of (V[:, 0..nv) | vec) and
-// call consume(stage, t0, rows) on each; all threads participate.
+// call consume(stage, vec_tile, t0, rows) on each; all threads participate,
+// thread 0 issues the copies.
 template <typename T, class F>
-__device__ __forceinline__ void stream_phase(Ring &R, int64_t rb, int64_t re, int TR, const T *V, int64_t ld, int nv,
+__device__ __forceinline__ void stream_phase(Ring &R, int64_t rb, int64_t re, const CUtensorMap *tmV, int nv,
                                              const T *vec, F &&consume) {
+    constexpr int TR = TileRows<T>::value;
+    const int nbox = (nv + kCB - 1) / kCB;
+    const size_t sbytes = ((size_t)(nbox * kCB + 1) * TR * sizeof(T) + 127) / 128 * 128;
+    int S = (int)(kRingBytes / sbytes);
+    if (S > kMaxStages) S = kMaxStages;
     const int ntiles = (re > rb) ? (int)((re - rb + TR - 1) / TR) : 0;
-    fence_proxy_async_all();   // generic writes (own rows of V, w) before TMA reads
+    fence_proxy_async_global();   // generic writes (own rows of V, w, w') before TMA reads
     __syncthreads();
     if (threadIdx.x == 0) {
-        const int pre = ntiles < kStages ? ntiles : kStages;
-        for (int i = 0; i < pre; ++i) ring_issue<T>(R, R.gt + i, TR, V, ld, nv, vec, rb + (int64_t)i * TR);
+        const int pre = ntiles < S ? ntiles : S;
+        for (int i = 0; i < pre; ++i) ring_issue<T>(R, i, sbytes, TR, tmV, nv, vec, rb + (int64_t)i * TR);
     }
     for (int i = 0; i < ntiles; ++i) {
-        const uint32_t g = R.gt + i;
-        const int slot = (int)(g % kStages);
-        mbar_wait(&R.full[slot], (g / kStages) & 1u);
+        const int slot = i % S;
+        mbar_wait(&R.full[slot], (R.phase >> slot) & 1u);
+        R.phase ^= 1u << slot;
         const int64_t t0 = rb + (int64_t)i * TR;
         const int rows = (int)((re - t0) < TR ? (re - t0) : TR);
-        consume(reinterpret_cast<const T *>(R.base + (size_t)slot * kStageBytes), t0, rows);
-        fence_proxy_async_all();   // generic reads of the stage before it is refilled
-        __syncthreads();
-        if (threadIdx.x == 0 && i + kStages < ntiles)
-            ring_issue<T>(R, g + kStages, TR, V, ld, nv, vec, rb + (int64_t)(i + kStages) * TR);
+        const T *st = reinterpret_cast<const T *>(R.base + (size_t)slot * sbytes);
+        consume(st, st + (int64_t)nbox * kCB * TR, t0, rows);
+        __syncthreads();          // every thread is done with the stage before it is refilled
+        if (threadIdx.x == 0 && i + S < ntiles)
+            ring_issue<T>(R, slot, sbytes, TR, tmV, nv, vec, rb + (int64_t)(i + S) * TR);
     }
-    R.gt += ntiles;
+}
+
+// Strided dot over columns c = c0, c0+P, ... < nc of stage[c][rr] * coef[c]
+// with four independent accumulators (combined in a fixed order).
+template <typename T>
+__device__ __forceinline__ T strided_combine(const T *stage, int TR, int rr, int c0, int P, int nc, const T *coef) {
+    T s0 = T(0), s1 = T(0), s2 = T(0), s3 = T(0);
+    int c = c0;
+    for (; c + 3 * P < nc; c += 4 * P) {
+        s0 += stage[(int64_t)c * TR + rr] * coef[c];
+        s1 += stage[(int64_t)(c + P) * TR + rr] * coef[c + P];
+        s2 += stage[(int64_t)(c + 2 * P) * TR + rr] * coef[c + 2 * P];
+        s3 += stage[(int64_t)(c + 3 * P) * TR + rr] * coef[c + 3 * P];
+    }
+    for (; c < nc; c += P) s0 += stage[(int64_t)c * TR + rr] * coef[c];
+    return (s0 + s1) + (s2 + s3);
 }
 
 // Row-wise s[rr] = sum_{c < nc} stage[c][rr] * coef[c] for rr < rows; calls
@@ -193,17 +211,11 @@ __device__ __forceinline__ void tile_rowcombine(const T *stage, int TR, int rows
                                                 Fin &&fin) {
     const int tid = threadIdx.x;
     if (TR >= kFB) {
-        for (int rr = tid; rr < rows; rr += kFB) {
-            T s = T(0);
-            for (int c = 0; c < nc; ++c) s += stage[(int64_t)c * TR + rr] * coef[c];
-            fin(rr, s);
-        }
+        for (int rr = tid; rr < rows; rr += kFB) fin(rr, strided_combine<T>(stage, TR, rr, 0, 1, nc, coef));
         return;
     }
     const int P = kFB / TR, rr = tid % TR, p = tid / TR;
-    T s = T(0);
-    for (int c = p; c < nc; c += P) s += stage[(int64_t)c * TR + rr] * coef[c];
-    spart[p * TR + rr] = s;
+    spart[p * TR + rr] = strided_combine<T>(stage, TR, rr, p, P, nc, coef);
     __syncthreads();
     if (p == 0 && rr < rows) {
         T t = spart[rr];
@@ -213,7 +225,7 @@ __device__ __forceinline__ void tile_rowcombine(const T *stage, int TR, int rows
 }
 
 // Column-wise acc[q] += sum_{rr < rows} stage[c][rr] * x[rr] for the warp's
-// columns c = warp + kFW*q < nc.
+// columns c = warp + kFW*q < nc (rows past `rows` are masked by x == 0).
 template <typename T>
 __device__ __forceinline__ void tile_coldots(const T *stage, int TR, int rows, int nc, const T *x, T (&acc)[kFQ]) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -222,29 +234,37 @@ __device__ __forceinline__ void tile_coldots(const T *stage, int TR, int rows, i
         const int c = warp + kFW * q;
         if (c < nc) {
             const T *col = stage + (int64_t)c * TR;
-            T s = T(0);
-            for (int rr = lane; rr < rows; rr += 32) s += col[rr] * x[rr];
-            acc[q] += s;
+            T s0 = T(0), s1 = T(0), s2 = T(0), s3 = T(0);
+            int rr = lane;
+            for (; rr + 96 < rows; rr += 128) {
+                s0 += col[rr] * x[rr];
+                s1 += col[rr + 32] * x[rr + 32];
+                s2 += col[rr + 64] * x[rr + 64];
+                s3 += col[rr + 96] * x[rr + 96];
+            }
+            for (; rr < rows; rr += 32) s0 += col[rr] * x[rr];
+            acc[q] += (s0 + s1) + (s2 + s3);
         }
     }
 }
 
 template <typename T, class Op>
-__global__ void __launch_bounds__(kFB, 1) k_cycle_fused(Op A, FusedArgs<T> a) {
+__global__ void __launch_bounds__(kFB, 1) k_cycle_fused(Op A, FusedArgs<T> a, const __grid_constant__ CUtensorMap tmV) {
     extern __shared__ __align__(128) unsigned char dsm_raw[];
+    constexpr int TR = TileRows<T>::value;
     const int m = a.m, ldr = m + 1;
     Ring R;
-    R.base = dsm_raw;                                                    // kStages * kStageBytes
-    R.full = reinterpret_cast<uint64_t *>(dsm_raw + kStages * kStageBytes);
-    R.gt = 0;
-    T *sR = reinterpret_cast<T *>(dsm_raw + kStages * kStageBytes + 64);  // (m+1) x m rotated columns
+    R.base = dsm_raw;                                                    // kRingBytes
+    R.full = reinterpret_cast<uint64_t *>(dsm_raw + kRingBytes);
+    R.phase = 0;
+    T *sR = reinterpret_cast<T *>(dsm_raw + kRingBytes + 8 * kMaxStages);   // (m+1) x m rotated columns
     T *scs = sR + (int64_t)ldr * m;
     T *ssn = scs + m;
     T *sg = ssn + m;                           // m + 1
     T *sc1 = sg + (m + 1);                     // kFSlots
     T *sc2 = sc1 + kFSlots;                    // kFSlots
     T *spart = sc2 + kFSlots;                  // kFB
-    T *sx = spart + kFB;                       // kMaxTR (w' of the tile)
+    T *sx = spart + kFB;                       // TR (w' of the tile)
     T *sred = sx + kMaxTR;                     // kFW
     __shared__ T s_gamma, s_beta, s_bn2;
     __shared__ int s_done, s_steps, s_break, s_app;
@@ -260,7 +280,7 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_fused(Op A, FusedArgs<T> a) {
     const bool lead = (blockIdx.x == 0);
 
     if (tid == 0) {
-        for (int i = 0; i < kStages; ++i) mbar_init(&R.full[i], 1);
+        for (int i = 0; i < kMaxStages; ++i) mbar_init(&R.full[i], 1);
         fence_mbar_init();
         const T gamma = RN<T>::sqrt_(__ldcg(a.rnorm2));
         s_gamma = gamma;
@@ -288,7 +308,6 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_fused(Op A, FusedArgs<T> a) {
         const T *src = (k == 0) ? a.r0 : a.wpp;
         const T dv = (k == 0) ? s_gamma : s_beta;
         T *vk = a.V + (int64_t)k * a.ld;
-        const int TR = tile_rows<T>(nc + 1);
         T acc[kFQ];
         // ---------------- phase A: v_k = src/dv, w = A v_k, ||w||^2 ; c1 = V^T w
         T an = T(0);
@@ -300,8 +319,8 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_fused(Op A, FusedArgs<T> a) {
         }
 #pragma unroll
         for (int q = 0; q < kFQ; ++q) acc[q] = T(0);
-        stream_phase<T>(R, rb, re, TR, a.V, a.ld, nc, a.w, [&](const T *st, int64_t, int rows) {
-            tile_coldots<T>(st, TR, rows, nc, st + (int64_t)nc * TR, acc);
+        stream_phase<T>(R, rb, re, &tmV, nc, a.w, [&](const T *st, const T *wv, int64_t, int rows) {
+            tile_coldots<T>(st, TR, rows, nc, wv, acc);
         });
         write_partials<T>(acc, nc, an, sred, partA);
         grid_sync(a.bar, nb);
@@ -310,8 +329,7 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_fused(Op A, FusedArgs<T> a) {
         // ---------------- phase B: w' = w - V c1 ; c2 = V^T w'
 #pragma unroll
         for (int q = 0; q < kFQ; ++q) acc[q] = T(0);
-        stream_phase<T>(R, rb, re, TR, a.V, a.ld, nc, a.w, [&](const T *st, int64_t t0, int rows) {
-            const T *wv = st + (int64_t)nc * TR;
+        stream_phase<T>(R, rb, re, &tmV, nc, a.w, [&](const T *st, const T *wv, int64_t t0, int rows) {
             tile_rowcombine<T>(st, TR, rows, nc, sc1, spart, [&](int rr, T s) {
                 const T wr = RN<T>::sub(wv[rr], s);
                 a.wp[t0 + rr] = wr;
@@ -326,8 +344,7 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_fused(Op A, FusedArgs<T> a) {
         __syncthreads();
         // ---------------- phase C: w'' = w' - V c2 ; ||w''||^2
         T bn = T(0);
-        stream_phase<T>(R, rb, re, TR, a.V, a.ld, nc, a.wp, [&](const T *st, int64_t t0, int rows) {
-            const T *wv = st + (int64_t)nc * TR;
+        stream_phase<T>(R, rb, re, &tmV, nc, a.wp, [&](const T *st, const T *wv, int64_t t0, int rows) {
             tile_rowcombine<T>(st, TR, rows, nc, sc2, spart, [&](int rr, T s) {
                 const T wr = RN<T>::sub(wv[rr], s);
                 a.wpp[t0 + rr] = wr;
@@ -453,9 +470,8 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_fused(Op A, FusedArgs<T> a) {
         for (int64_t r = rb + tid; r < re; r += kFB) a.x_out[r] = a.x0[r];
         return;
     }
-    const int TRe = tile_rows<T>(k);
-    stream_phase<T>(R, rb, re, TRe, a.V, a.ld, k, (const T *)nullptr, [&](const T *st, int64_t t0, int rows) {
-        tile_rowcombine<T>(st, TRe, rows, k, sd, spart, [&](int rr, T s) {
+    stream_phase<T>(R, rb, re, &tmV, k, (const T *)nullptr, [&](const T *st, const T *, int64_t t0, int rows) {
+        tile_rowcombine<T>(st, TR, rows, k, sd, spart, [&](int rr, T s) {
             a.x_out[t0 + rr] = RN<T>::add(a.x0[t0 + rr], s);
         });
     });

@@ -1,6 +1,7 @@
 // Bulk-async copy (TMA engine, cp.async.bulk) + mbarrier helpers for sm_100a.
 #pragma once
 
+#include <cuda.h>
 #include <stdint.h>
 
 namespace mpk {
@@ -45,9 +46,19 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         : "memory");
 }
 
-// order this thread's generic-proxy accesses before later async-proxy ones
-__device__ __forceinline__ void fence_proxy_async_all() {
-    asm volatile("fence.proxy.async;" ::: "memory");
+// 2-D tensor-map load of one box at coordinates (x = row, y = column)
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *tmap, int x, int y, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// order this thread's generic-proxy global writes before later async-proxy
+// (bulk copy) reads of them
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 __device__ __forceinline__ void fence_mbar_init() {

@@ -52,7 +52,8 @@ class CycleWorkspace:
         # zero-initialised: rows [n, ld) of every column stay zero (the fused
         # kernel's 16-byte row groups and chunk tails read them)
         self.V = t.zeros((self.m + 1) * self.ld, dtype=td, device=dev)
-        self.work = t.zeros(4 * self.ld, dtype=td, device=dev)
+        # + 512 elements: 1-D bulk copies of a 256-row tile may run past w''s ld
+        self.work = t.zeros(4 * self.ld + 512, dtype=td, device=dev)
         self.hess = t.zeros(int(lib.mpk_cycle_hess_bytes(self.m, prec.code)), dtype=t.uint8, device=dev)
         self.ws = D.ReduceWorkspace()
         self.ctlbuf = t.zeros(CTLBUF_BYTES, dtype=t.uint8, device=dev)
