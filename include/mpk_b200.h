@@ -191,7 +191,8 @@ typedef struct mpk_cycle_desc {
     mpk_cycle_ctl *ctl;     /* device */
     int32_t nranks;         /* 1 (multi-rank cycles go through mpk_cycle_step_*) */
     int32_t flags;          /* bit0: per-kernel event timing; bit1: write the last basis column;
-                               bit2: force the multi-kernel cycle (no persistent kernel) */
+                               bit2: force the multi-kernel cycle (no persistent kernel);
+                               bit3: phase profiler of the persistent kernel */
 } mpk_cycle_desc;
 
 int64_t mpk_cycle_hess_bytes(int32_t m, int32_t dtype);
@@ -242,6 +243,9 @@ int mpk_prof_reset(void);
 int64_t mpk_launch_count(void);
 /* totals[c] = summed milliseconds, counts[c] = launches, bytes[c] = algorithmic bytes */
 int mpk_prof_read(double *ms, int64_t *counts, double *bytes, int32_t nclasses);
+/* per-CTA clock64 totals of the persistent cycle's sections (16 slots per
+ * CTA) from the last cycle run with flag bit3 */
+int mpk_fused_prof_read(uint64_t *out, int32_t nctas);
 
 #ifdef __cplusplus
 }

@@ -27,7 +27,7 @@ EXPORTS = (
     "mpk_reduce_ws_bytes", "mpk_dot", "mpk_norm2", "mpk_axpy", "mpk_scale", "mpk_cgs2_append",
     "mpk_cycle_hess_bytes", "mpk_cycle_run", "mpk_residual", "mpk_ir_update",
     "mpk_precond_apply", "mpk_prof_reset", "mpk_prof_read", "mpk_lsq_init", "mpk_lsq_update",
-    "mpk_lsq_solve", "mpk_vdiv", "mpk_launch_count",
+    "mpk_lsq_solve", "mpk_vdiv", "mpk_launch_count", "mpk_fused_prof_read",
 )
 
 
@@ -105,6 +105,7 @@ _SIGS = {
                              ctypes.POINTER(ctypes.c_double), _I32]),
 }
 _SIGS["mpk_launch_count"] = (_I64, [])
+_SIGS["mpk_fused_prof_read"] = (_I32, [ctypes.POINTER(ctypes.c_uint64), _I32])
 _SIGS["mpk_vdiv"] = (_I32, [_I32, _I64, _P, _P, _P, _P])
 _SIGS["mpk_lsq_init"] = (_I32, [_I32, _I32, ctypes.c_double, ctypes.c_double, _P, _P, _P])
 _SIGS["mpk_lsq_update"] = (_I32, [_I32, _I32, _I32, _P, _P, _P, _P, _P, _P])

@@ -9,6 +9,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -16,7 +17,7 @@
 #include <utility>
 #include <vector>
 
-#include "fused.cuh"
+#include "fused_reg.cuh"
 
 using namespace mpk;
 
@@ -511,6 +512,145 @@ int encode_basis_map(CUtensorMap *map, const void *V, int64_t ld, int ncols, int
     return MPK_OK;
 }
 
+// Rows per TMA tile of the fused cycle (64, 128 or 256): 512 bytes of each
+// column per tile by default (128 fp32 / 64 fp64 rows; a 51-column stage is
+// ~33 KB, so the ring keeps 4-5 stages in flight).  MPK_FUSED_TR overrides.
+int fused_tile_rows(int sv) {
+    static int rows = -1;
+    if (rows < 0) {
+        const char *e = getenv("MPK_FUSED_TR");
+        rows = e ? atoi(e) : 0;
+        if (rows != 64 && rows != 128 && rows != 256) rows = 0;
+    }
+    return rows ? rows : 512 / sv;
+}
+
+template <typename T, class Op, int TR>
+int launch_fused(const Op &op, const mpk_cycle_desc *d, int cap, double tf, double u, cudaStream_t s) {
+    static_assert(TR <= kMaxTR, "tile rows");
+    const int m = d->m;
+    T *w = (T *)d->work;
+    Ws ws = carve(d->ws);
+    auto kern = k_cycle_fused<T, Op, TR>;
+    const size_t smem = (size_t)kRingBytes + 8 * kMaxStages +
+                        sizeof(T) * ((size_t)(m + 1) * m + 2 * m + (m + 1) + 2 * kFSlots + kFB + kMaxTR + kFW);
+    CUtensorMap tmap;
+    int erc = encode_basis_map(&tmap, d->V, d->ld, m + 1, (int)sizeof(T), TR);
+    if (erc) return erc;
+    static size_t attr_set = 0;
+    if (smem > attr_set) {
+        cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (ea != cudaSuccess) {
+            g_err = std::string("k_cycle_fused smem attribute: ") + cudaGetErrorString(ea);
+            return MPK_ELAUNCH;
+        }
+        attr_set = smem;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFB, smem);
+    if (per_sm < 1) return fail(MPK_ELAUNCH, "fused cycle kernel does not fit on an SM");
+    int grid = sm_count_cached();
+    if (grid > kFMaxCtas) grid = kFMaxCtas;
+    FusedArgs<T> fa;
+    fa.n = d->n;
+    fa.ld = d->ld;
+    fa.m = m;
+    fa.cap = cap;
+    fa.V = (T *)d->V;
+    fa.r0 = (const T *)d->r0;
+    fa.rnorm2 = (const T *)d->rnorm2;
+    fa.x0 = (const T *)d->x0;
+    fa.x_out = (T *)d->x_out;
+    fa.w = w;
+    fa.wp = w + d->ld;
+    fa.wpp = w + 2 * d->ld;
+    fa.part = (T *)ws.partials;
+    fa.bar = ws.counters + 8;
+    fa.H = hess_view<T>(d->hess, m);
+    fa.ctl = d->ctl;
+    fa.tf = tf;
+    fa.exit_tol = d->exit_tol;
+    fa.norm_scale = d->norm_scale;
+    fa.u = u;
+    fa.final_col = (d->flags & 2) ? 1 : 0;
+    fa.prof = (d->flags & 8) ? 1 : 0;
+    Op opc = op;
+    void *args[] = {(void *)&opc, (void *)&fa, (void *)&tmap};
+    ProfScope ps(7, 0.0, s);
+    cudaError_t e = cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(kFB), args, smem, s);
+    if (e != cudaSuccess) {
+        g_err = std::string("k_cycle_fused: ") + cudaGetErrorString(e);
+        return MPK_ELAUNCH;
+    }
+    return check_launch("k_cycle_fused");
+}
+
+// Persistent cycle variant: "reg" (16-byte register streaming, default) or
+// "tma" (TMA ring through shared memory); MPK_FUSED_IMPL overrides.
+bool fused_use_tma() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("MPK_FUSED_IMPL");
+        v = (e && strcmp(e, "tma") == 0) ? 1 : 0;
+    }
+    return v == 1;
+}
+
+template <typename T, class Op>
+int launch_fused_reg(const Op &op, const mpk_cycle_desc *d, int cap, double tf, double u, cudaStream_t s) {
+    const int m = d->m;
+    T *w = (T *)d->work;
+    Ws ws = carve(d->ws);
+    auto kern = k_cycle_reg<T, Op>;
+    const size_t smem = sizeof(T) * ((size_t)(m + 1) * m + 2 * m + (m + 1) + 2 * kFSlots + kFW * kFSlots);
+    static size_t attr_set = 0;
+    if (smem > attr_set) {
+        cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (ea != cudaSuccess) {
+            g_err = std::string("k_cycle_reg smem attribute: ") + cudaGetErrorString(ea);
+            return MPK_ELAUNCH;
+        }
+        attr_set = smem;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFB, smem);
+    if (per_sm < 1) return fail(MPK_ELAUNCH, "register cycle kernel does not fit on an SM");
+    int grid = sm_count_cached();
+    if (grid > kFMaxCtas) grid = kFMaxCtas;
+    FusedArgs<T> fa;
+    fa.n = d->n;
+    fa.ld = d->ld;
+    fa.m = m;
+    fa.cap = cap;
+    fa.V = (T *)d->V;
+    fa.r0 = (const T *)d->r0;
+    fa.rnorm2 = (const T *)d->rnorm2;
+    fa.x0 = (const T *)d->x0;
+    fa.x_out = (T *)d->x_out;
+    fa.w = w;
+    fa.wp = w + d->ld;
+    fa.wpp = w + 2 * d->ld;
+    fa.part = (T *)ws.partials;
+    fa.bar = ws.counters + 8;
+    fa.H = hess_view<T>(d->hess, m);
+    fa.ctl = d->ctl;
+    fa.tf = tf;
+    fa.exit_tol = d->exit_tol;
+    fa.norm_scale = d->norm_scale;
+    fa.u = u;
+    fa.final_col = (d->flags & 2) ? 1 : 0;
+    fa.prof = (d->flags & 8) ? 1 : 0;
+    Op opc = op;
+    void *args[] = {(void *)&opc, (void *)&fa};
+    ProfScope ps(7, 0.0, s);
+    cudaError_t e = cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(kFB), args, smem, s);
+    if (e != cudaSuccess) {
+        g_err = std::string("k_cycle_reg: ") + cudaGetErrorString(e);
+        return MPK_ELAUNCH;
+    }
+    return check_launch("k_cycle_reg");
+}
+
 template <typename T> int run_cycle(const mpk_cycle_desc *d, cudaStream_t s) {
     const int64_t n = d->n, ld = d->ld;
     const int m = d->m;
@@ -533,57 +673,13 @@ template <typename T> int run_cycle(const mpk_cycle_desc *d, cudaStream_t s) {
         // persistent cooperative cycle: one launch for the whole cycle
         return with_op<T>(d->A, [&](auto op) -> int {
             using Op = decltype(op);
-            auto kern = k_cycle_fused<T, Op>;
-            const size_t smem = (size_t)kRingBytes + 8 * kMaxStages +
-                                sizeof(T) * ((size_t)(m + 1) * m + 2 * m + (m + 1) + 2 * kFSlots + kFB +
-                                             TileRows<T>::value + kFW);
-            CUtensorMap tmap;
-            int erc = encode_basis_map(&tmap, V, ld, m + 1, (int)sizeof(T), TileRows<T>::value);
-            if (erc) return erc;
-            static size_t attr_set = 0;
-            if (smem > attr_set) {
-                cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                if (ea != cudaSuccess) {
-                    g_err = std::string("k_cycle_fused smem attribute: ") + cudaGetErrorString(ea);
-                    return MPK_ELAUNCH;
-                }
-                attr_set = smem;
-            }
-            int per_sm = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFB, smem);
-            if (per_sm < 1) return fail(MPK_ELAUNCH, "fused cycle kernel does not fit on an SM");
-            int grid = sm_count_cached() * (per_sm > 1 ? 1 : per_sm);
-            if (grid > kFMaxCtas) grid = kFMaxCtas;
-            FusedArgs<T> fa;
-            fa.n = n;
-            fa.ld = ld;
-            fa.m = m;
-            fa.cap = cap;
-            fa.V = V;
-            fa.r0 = (const T *)d->r0;
-            fa.rnorm2 = (const T *)d->rnorm2;
-            fa.x0 = (const T *)d->x0;
-            fa.x_out = (T *)d->x_out;
-            fa.w = w;
-            fa.wp = wp;
-            fa.wpp = wpp;
-            fa.part = (T *)ws.partials;
-            fa.bar = ws.counters + 8;
-            fa.H = H;
-            fa.ctl = ctl;
-            fa.tf = tf;
-            fa.exit_tol = d->exit_tol;
-            fa.norm_scale = d->norm_scale;
-            fa.u = u;
-            fa.final_col = (d->flags & 2) ? 1 : 0;
-            void *args[] = {(void *)&op, (void *)&fa, (void *)&tmap};
-            ProfScope ps(7, 0.0, s);
-            cudaError_t e = cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(kFB), args, smem, s);
-            if (e != cudaSuccess) {
-                g_err = std::string("k_cycle_fused: ") + cudaGetErrorString(e);
-                return MPK_ELAUNCH;
-            }
-            return check_launch("k_cycle_fused");
+            const bool aligned = ((uintptr_t)d->x_out % 16 == 0) && ((uintptr_t)d->V % 16 == 0) &&
+                                 ((uintptr_t)d->work % 16 == 0) && ((uintptr_t)d->r0 % 16 == 0);
+            if (!fused_use_tma() && aligned && m + 1 <= kRegMaxCols) return launch_fused_reg<T, Op>(op, d, cap, tf, u, s);
+            const int tr = fused_tile_rows(sizeof(T));
+            if (tr == 256) return launch_fused<T, Op, 256>(op, d, cap, tf, u, s);
+            if (tr == 64) return launch_fused<T, Op, 64>(op, d, cap, tf, u, s);
+            return launch_fused<T, Op, 128>(op, d, cap, tf, u, s);
         });
     }
 
@@ -921,6 +1017,13 @@ int mpk_prof_reset(void) {
         g_prof_cnt[i] = 0;
         g_prof_bytes[i] = 0;
     }
+    return MPK_OK;
+}
+
+int mpk_fused_prof_read(uint64_t *out, int32_t nctas) {
+    if (nctas > kFMaxCtas) nctas = kFMaxCtas;
+    cudaError_t e = cudaMemcpyFromSymbol(out, g_fused_prof, sizeof(uint64_t) * kProfSlots * nctas);
+    if (e != cudaSuccess) return fail(MPK_ELAUNCH, cudaGetErrorString(e));
     return MPK_OK;
 }
 

