@@ -249,7 +249,7 @@ def main():
     alg = sum(sum(spmv_b + sv * n * (4 * (k + 1) + 10) for k in range(st)) + sv * n * (st + 2)
               for st in steps_per_cycle) * args.steps
     names = ["spmv+norm+dot1", "update1+dot2", "update2+norm+givens", "normalise", "precond",
-             "correction", "residual", "fused Arnoldi cycle (k_cycle_fused)"]
+             "correction", "residual", "persistent Arnoldi cycle (k_cycle_reg)"]
     kern = {}
     for i in range(NC):
         if pc[i]:
@@ -259,6 +259,8 @@ def main():
     top = max(range(NC), key=lambda i: pm[i])
     peak, peak_kind = peaks()
     achieved = (alg if top == 7 else pb[top]) / (pm[top] * 1e-3) / 1e9
+    # ncu DRAM bytes per launch of the cycle kernel (one 50-step cycle), from
+    # profiles/traffic_<config>.json (ncu --set full of the same kernel)
     traffic = None
     prof = os.path.join(ROOT, "profiles", "traffic_%s.json" % args.config)
     if os.path.exists(prof):
@@ -266,6 +268,11 @@ def main():
             traffic = json.load(open(prof)).get("bytes_per_launch")
         except Exception:
             traffic = None
+    traffic_gbs = None
+    if traffic and top == 7 and pc[7]:
+        full = [st for st in steps_per_cycle if st == 50]
+        if len(full) == len(steps_per_cycle):   # every launch is a full cycle
+            traffic_gbs = traffic / (pm[7] * 1e-3 / pc[7]) / 1e9
 
     out = {
         "metric": "GMRES-IR time-to-1e-10 residual (s)",
@@ -288,6 +295,11 @@ def main():
         "kernels": kern,
         "roofline": {"bound": "hbm", "kernel": names[top], "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     "traffic_GBs": traffic_gbs,
+                     "traffic_frac": (traffic_gbs / peak) if traffic_gbs else None,
+                     "note": "achieved = SURVEY 8(d) algorithmic bytes (two CGS2 GEMV pairs = 4 passes over V); "
+                             "the kernel reads V 3 times per step, so traffic_GBs (ncu DRAM bytes per launch / "
+                             "mean launch time) is the physical HBM rate",
                      "algorithmic_bytes": "per step: stencil SpMV 2*4*n + CGS2 4*n*(4j+10); "
                                           "per cycle: correction 4*n*(k+2) (SURVEY 8(d))"},
     }
