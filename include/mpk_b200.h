@@ -151,6 +151,44 @@ int mpk_cgs2_append(int32_t dtype, int64_t n, int64_t ld, int32_t count, void *V
                     void *ws, void *stream);
 
 /* ------------------------------------------------------------------ */
+/* row-partitioned multi-GPU cycle                       */
+/* ------------------------------------------------------------------ */
+/* One rank per GPU owns the contiguous global rows [row0, row0 + n).  The
+ * persistent cycle kernel of every rank writes its per-CTA dot-product
+ * partials straight into every rank's partial buffer and its boundary rows
+ * of w'' straight into the neighbours' global-length x buffers (P2P stores
+ * over NVLink through CUDA-IPC-mapped pointers), then meets the other ranks
+ * at a system-scope counter barrier; every rank reduces all ranks' partials
+ * in the same fixed order and runs the same Givens update, so the cycle
+ * needs no NCCL call and no host round trip.  Pointers below are indexed by
+ * rank; the local rank's entries are its own buffers. */
+#define MPK_MAX_RANKS 8
+typedef struct mpk_comm {
+    int32_t rank;
+    int32_t nranks;
+    int32_t ctas;                    /* CTAs of each rank's cycle kernel (0 = one per SM) */
+    int32_t pad_;
+    int64_t row0;                    /* first global row of this rank */
+    void *part[MPK_MAX_RANKS];       /* mpk_comm_part_bytes(dtype) each */
+    void *xbar[MPK_MAX_RANKS];       /* uint64 arrival counter each (zero-initialised) */
+    void *epoch;                     /* uint64, this rank's barriers so far (zero-initialised) */
+    void *xg[MPK_MAX_RANKS];         /* global-length vector (cycle dtype, global row 0) each */
+    int64_t mir_lo[MPK_MAX_RANKS];   /* local rows [mir_lo[q], mir_hi[q]) of w'' are mirrored */
+    int64_t mir_hi[MPK_MAX_RANKS];   /*   into rank q's xg (q != rank; empty: lo >= hi) */
+} mpk_comm;
+
+/* bytes of one rank's partial buffer (3 phases x 65 slots x 8 ranks x 320 CTAs) */
+int64_t mpk_comm_part_bytes(int32_t dtype);
+/* cudaMalloc'd (not pool) memory, so that CUDA IPC handles cover it exactly */
+int mpk_dev_alloc(int64_t bytes, void **ptr);
+int mpk_dev_free(void *ptr);
+/* 64-byte cudaIpcMemHandle_t of an mpk_dev_alloc pointer, and its mapping in
+ * another process (cudaIpcMemLazyEnablePeerAccess) */
+int mpk_ipc_get(const void *ptr, void *handle64);
+int mpk_ipc_open(const void *handle64, void **ptr);
+int mpk_ipc_close(void *ptr);
+
+/* ------------------------------------------------------------------ */
 /* restarted GMRES cycle (gmres.py:134-205)                            */
 /* ------------------------------------------------------------------ */
 /* Device control block of one cycle (read back once per cycle). */
@@ -189,10 +227,11 @@ typedef struct mpk_cycle_desc {
     void *hess;             /* mpk_cycle_hess_bytes(m, dtype) */
     void *ws;               /* mpk_reduce_ws_bytes(n, m + 2) */
     mpk_cycle_ctl *ctl;     /* device */
-    int32_t nranks;         /* 1 (multi-rank cycles go through mpk_cycle_step_*) */
+    int32_t nranks;         /* 1, or > 1 with `comm` (row-partitioned; identity preconditioner) */
     int32_t flags;          /* bit0: per-kernel event timing; bit1: write the last basis column;
                                bit2: force the multi-kernel cycle (no persistent kernel);
                                bit3: phase profiler of the persistent kernel */
+    const mpk_comm *comm;   /* nranks > 1: this rank's view of the communicator */
 } mpk_cycle_desc;
 
 int64_t mpk_cycle_hess_bytes(int32_t m, int32_t dtype);

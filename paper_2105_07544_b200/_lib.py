@@ -27,8 +27,10 @@ EXPORTS = (
     "mpk_reduce_ws_bytes", "mpk_dot", "mpk_norm2", "mpk_axpy", "mpk_scale", "mpk_cgs2_append",
     "mpk_cycle_hess_bytes", "mpk_cycle_run", "mpk_residual", "mpk_ir_update",
     "mpk_precond_apply", "mpk_prof_reset", "mpk_prof_read", "mpk_lsq_init", "mpk_lsq_update",
-    "mpk_lsq_solve", "mpk_vdiv", "mpk_launch_count", "mpk_fused_prof_read",
+    "mpk_lsq_solve", "mpk_vdiv", "mpk_launch_count", "mpk_fused_prof_read", "mpk_comm_part_bytes",
+    "mpk_dev_alloc", "mpk_dev_free", "mpk_ipc_get", "mpk_ipc_open", "mpk_ipc_close",
 )
+MAX_RANKS = 8
 
 
 class NativeUnavailable(RuntimeError):
@@ -65,6 +67,16 @@ class MpkCycleCtl(ctypes.Structure):
     ]
 
 
+class MpkComm(ctypes.Structure):
+    _fields_ = [
+        ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("ctas", ctypes.c_int32),
+        ("pad_", ctypes.c_int32), ("row0", ctypes.c_int64),
+        ("part", ctypes.c_void_p * MAX_RANKS), ("xbar", ctypes.c_void_p * MAX_RANKS),
+        ("epoch", ctypes.c_void_p), ("xg", ctypes.c_void_p * MAX_RANKS),
+        ("mir_lo", ctypes.c_int64 * MAX_RANKS), ("mir_hi", ctypes.c_int64 * MAX_RANKS),
+    ]
+
+
 class MpkCycleDesc(ctypes.Structure):
     _fields_ = [
         ("A", ctypes.POINTER(MpkMatrix)), ("M", ctypes.POINTER(MpkPrecond)),
@@ -74,7 +86,7 @@ class MpkCycleDesc(ctypes.Structure):
         ("r0", ctypes.c_void_p), ("rnorm2", ctypes.c_void_p), ("x0", ctypes.c_void_p),
         ("x_out", ctypes.c_void_p), ("work", ctypes.c_void_p), ("hess", ctypes.c_void_p),
         ("ws", ctypes.c_void_p), ("ctl", ctypes.c_void_p), ("nranks", ctypes.c_int32),
-        ("flags", ctypes.c_int32),
+        ("flags", ctypes.c_int32), ("comm", ctypes.POINTER(MpkComm)),
     ]
 
 
@@ -106,6 +118,12 @@ _SIGS = {
 }
 _SIGS["mpk_launch_count"] = (_I64, [])
 _SIGS["mpk_fused_prof_read"] = (_I32, [ctypes.POINTER(ctypes.c_uint64), _I32])
+_SIGS["mpk_comm_part_bytes"] = (_I64, [_I32])
+_SIGS["mpk_dev_alloc"] = (_I32, [_I64, ctypes.POINTER(ctypes.c_void_p)])
+_SIGS["mpk_dev_free"] = (_I32, [_P])
+_SIGS["mpk_ipc_get"] = (_I32, [_P, _P])
+_SIGS["mpk_ipc_open"] = (_I32, [_P, ctypes.POINTER(ctypes.c_void_p)])
+_SIGS["mpk_ipc_close"] = (_I32, [_P])
 _SIGS["mpk_vdiv"] = (_I32, [_I32, _I64, _P, _P, _P, _P])
 _SIGS["mpk_lsq_init"] = (_I32, [_I32, _I32, ctypes.c_double, ctypes.c_double, _P, _P, _P])
 _SIGS["mpk_lsq_update"] = (_I32, [_I32, _I32, _I32, _P, _P, _P, _P, _P, _P])

@@ -640,6 +640,29 @@ int launch_fused_reg(const Op &op, const mpk_cycle_desc *d, int cap, double tf, 
     fa.u = u;
     fa.final_col = (d->flags & 2) ? 1 : 0;
     fa.prof = (d->flags & 8) ? 1 : 0;
+    memset(&fa.cm, 0, sizeof(fa.cm));
+    fa.cm.nranks = 1;
+    if (d->nranks > 1) {
+        const mpk_comm *c = d->comm;
+        if (!c || c->nranks != d->nranks || c->nranks > kMaxRanks || c->rank < 0 || c->rank >= c->nranks)
+            return fail(MPK_EARG, "multi-rank cycle needs a consistent mpk_comm");
+        fa.cm.rank = c->rank;
+        fa.cm.nranks = c->nranks;
+        fa.cm.row0 = c->row0;
+        fa.cm.epoch = (unsigned long long *)c->epoch;
+        for (int q = 0; q < c->nranks; ++q) {
+            fa.cm.part[q] = (T *)c->part[q];
+            fa.cm.xbar[q] = (unsigned long long *)c->xbar[q];
+            fa.cm.xg[q] = (T *)c->xg[q];
+            fa.cm.mir_lo[q] = c->mir_lo[q];
+            fa.cm.mir_hi[q] = c->mir_hi[q];
+            if (!fa.cm.part[q] || !fa.cm.xbar[q] || !fa.cm.xg[q]) return fail(MPK_EARG, "null peer pointer");
+        }
+        if (c->row0 % 64 != 0 || ((uintptr_t)c->xg[c->rank] % 16) != 0)
+            return fail(MPK_EARG, "rank row blocks must start on 64-row boundaries");
+        fa.wpp = (T *)c->xg[c->rank] + c->row0;   // w'' lives in the rank's global-length vector
+        if (c->ctas > 0 && c->ctas < grid) grid = c->ctas;
+    }
     Op opc = op;
     void *args[] = {(void *)&opc, (void *)&fa};
     ProfScope ps(7, 0.0, s);
@@ -669,7 +692,16 @@ template <typename T> int run_cycle(const mpk_cycle_desc *d, cudaStream_t s) {
     const double tf = (d->rule == MPK_RULE_U) ? u : (double)n * u;   // kernels.py:122
     int rc;
 
-    if (!precond && m + 1 <= kFMaxCols && d->nranks <= 1 && !(d->flags & 4)) {
+    if (d->nranks > 1) {
+        if (precond || m + 1 > kRegMaxCols || (uintptr_t)d->x_out % 16 || (uintptr_t)d->V % 16 ||
+            (uintptr_t)d->work % 16 || (uintptr_t)d->r0 % 16)
+            return fail(MPK_EUNSUPPORTED, "row-partitioned cycle: identity preconditioner, m <= 51, "
+                                          "16-byte aligned buffers");
+        return with_op<T>(d->A, [&](auto op) -> int {
+            return launch_fused_reg<T, decltype(op)>(op, d, cap, tf, u, s);
+        });
+    }
+    if (!precond && m + 1 <= kFMaxCols && !(d->flags & 4)) {
         // persistent cooperative cycle: one launch for the whole cycle
         return with_op<T>(d->A, [&](auto op) -> int {
             using Op = decltype(op);
@@ -1018,6 +1050,45 @@ int mpk_prof_reset(void) {
         g_prof_bytes[i] = 0;
     }
     return MPK_OK;
+}
+
+int64_t mpk_comm_part_bytes(int32_t dtype) {
+    return 3LL * kFSlots * kXStride * (dtype == MPK_F64 ? 8 : 4);
+}
+
+int mpk_dev_alloc(int64_t bytes, void **ptr) {
+    if (!ptr || bytes <= 0) return fail(MPK_EARG, "mpk_dev_alloc: bad arguments");
+    cudaError_t e = cudaMalloc(ptr, (size_t)bytes);
+    if (e != cudaSuccess) return fail(MPK_ELAUNCH, cudaGetErrorString(e));
+    e = cudaMemset(*ptr, 0, (size_t)bytes);
+    if (e != cudaSuccess) return fail(MPK_ELAUNCH, cudaGetErrorString(e));
+    return MPK_OK;
+}
+
+int mpk_dev_free(void *ptr) {
+    cudaError_t e = cudaFree(ptr);
+    return e == cudaSuccess ? MPK_OK : fail(MPK_ELAUNCH, cudaGetErrorString(e));
+}
+
+int mpk_ipc_get(const void *ptr, void *handle64) {
+    cudaIpcMemHandle_t h;
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void *>(ptr));
+    if (e != cudaSuccess) return fail(MPK_ELAUNCH, cudaGetErrorString(e));
+    memcpy(handle64, &h, sizeof(h));
+    return MPK_OK;
+}
+
+int mpk_ipc_open(const void *handle64, void **ptr) {
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle64, sizeof(h));
+    cudaError_t e = cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    return e == cudaSuccess ? MPK_OK : fail(MPK_ELAUNCH, cudaGetErrorString(e));
+}
+
+int mpk_ipc_close(void *ptr) {
+    cudaError_t e = cudaIpcCloseMemHandle(ptr);
+    return e == cudaSuccess ? MPK_OK : fail(MPK_ELAUNCH, cudaGetErrorString(e));
 }
 
 int mpk_fused_prof_read(uint64_t *out, int32_t nctas) {

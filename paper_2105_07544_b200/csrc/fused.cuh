@@ -45,6 +45,22 @@ constexpr int kRingBytes = 176 * 1024;  // shared memory of the ring
 constexpr int kCB = 16;                 // basis columns per tensor-map box
 constexpr int kMaxTR = 256;             // rows per tile, upper bound (TR is a template parameter)
 
+// Row-partitioned multi-GPU cycle (one process per GPU, or virtual ranks
+// sharing one GPU in tests): peer pointers to every rank's partial buffer,
+// arrival counter and global-length x buffer (all P2P-mapped; for the local
+// rank they are its own).  See k_cycle_reg.
+constexpr int kMaxRanks = MPK_MAX_RANKS;
+constexpr int kXStride = kMaxRanks * kFMaxCtas;   // partial columns: rank * nb + cta
+template <typename T> struct CommArgs {
+    int rank, nranks;
+    T *part[kMaxRanks];                      // 3 phases x kFSlots x kXStride
+    unsigned long long *xbar[kMaxRanks];     // arrival counters (monotonic)
+    unsigned long long *epoch;               // own barriers completed (persists across launches)
+    T *xg[kMaxRanks];                        // global-length vectors, global row 0
+    int64_t row0;                            // first global row of this rank
+    int64_t mir_lo[kMaxRanks], mir_hi[kMaxRanks];   // own local rows mirrored into rank q's xg
+};
+
 template <typename T> struct FusedArgs {
     int64_t n, ld;
     int m, cap;
@@ -61,6 +77,7 @@ template <typename T> struct FusedArgs {
     double tf, exit_tol, norm_scale, u;
     int final_col;    // collect_basis: also write V[:, steps] = w''/beta
     int prof;         // phase profiler on
+    CommArgs<T> cm;   // nranks > 1: row-partitioned cycle
 };
 
 // Phase profiler (desc flag bit 3): per-CTA clock64 totals of each section,
@@ -89,27 +106,79 @@ __device__ __forceinline__ void grid_sync(unsigned *bar, unsigned nb) {
     __syncthreads();
 }
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Grid barrier spanning all ranks: local arrival as in grid_sync; the last
+// local CTA publishes the rank's arrival to every rank's counter (system-
+// scope atomics through the P2P mapping) and waits until its own counter
+// shows all ranks' arrivals for barrier number `target`, then releases the
+// local CTAs.  The fences order every CTA's P2P partial/halo stores before
+// the arrival.  A rank that never arrives (crashed peer, or virtual ranks
+// not co-resident) trips a 20 s timeout instead of hanging the GPU: bar[2]
+// is set and every CTA returns true (abort).
+template <typename T>
+__device__ __forceinline__ bool grid_sync_x(unsigned *bar, unsigned nb, const CommArgs<T> &cm,
+                                            unsigned long long target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned *vgen = bar + 1;
+        const unsigned g0 = *vgen;
+        __threadfence_system();
+        if (atomicAdd(bar, 1u) == nb - 1) {
+            bar[0] = 0u;
+            __threadfence_system();
+            for (int q = 0; q < cm.nranks; ++q) atomicAdd_system(cm.xbar[q], 1ull);
+            volatile unsigned long long *mine = cm.xbar[cm.rank];
+            const unsigned long long need = (unsigned long long)cm.nranks * target;
+            const unsigned long long t0 = globaltimer_ns();
+            while (*mine < need) {
+                __nanosleep(64);
+                if (globaltimer_ns() - t0 > 20000000000ull) {
+                    atomicExch(bar + 2, 1u);
+                    break;
+                }
+            }
+            __threadfence_system();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*vgen == g0) __nanosleep(32);
+        }
+        __threadfence_system();
+    }
+    __syncthreads();
+    return *(volatile unsigned *)(bar + 2) != 0u;
+}
+
 // out[s] = sum over CTAs b (fixed order) of part[idx(s)][b], for slots
 // s < nslots, idx(s) = s for s < ncols else kFExtra.  One warp per slot,
 // lanes stride the CTAs, then a fixed butterfly: identical in every CTA.
 template <typename T>
-__device__ __forceinline__ void cross_reduce(const T *part, unsigned nb, int ncols, int nslots, T *out) {
+__device__ __forceinline__ void cross_reduce(const T *part, unsigned nb, int ncols, int nslots, T *out,
+                                             int stride = kFMaxCtas) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
     for (int q = 0; q < (kFSlots + kFW - 1) / kFW; ++q) {
         const int s = warp + kFW * q;
         if (s < nslots) {
             const int idx = (s < ncols) ? s : kFExtra;
-            const T *p = part + (int64_t)idx * kFMaxCtas;
-            T v[kFMaxCtas / 32];
-#pragma unroll
-            for (int i = 0; i < kFMaxCtas / 32; ++i) {
-                const unsigned b = lane + 32 * i;
-                v[i] = (b < nb) ? __ldcg(p + b) : T(0);
-            }
+            const T *p = part + (int64_t)idx * stride;
             T acc = T(0);
+            if (nb <= (unsigned)kFMaxCtas) {
+                T v[kFMaxCtas / 32];
 #pragma unroll
-            for (int i = 0; i < kFMaxCtas / 32; ++i) acc += v[i];
+                for (int i = 0; i < kFMaxCtas / 32; ++i) {
+                    const unsigned b = lane + 32 * i;
+                    v[i] = (b < nb) ? __ldcg(p + b) : T(0);
+                }
+#pragma unroll
+                for (int i = 0; i < kFMaxCtas / 32; ++i) acc += v[i];
+            } else {   // multi-rank: nb = nranks * CTAs per rank columns, same fixed order
+                for (unsigned b = lane; b < nb; b += 32) acc += __ldcg(p + b);
+            }
             acc = warp_sum(acc);
             if (lane == 0) out[s] = acc;
         }

@@ -66,7 +66,8 @@ enum { kRegDots = 0, kRegUpdateDots = 1, kRegUpdateNorm = 2, kRegCorrect = 3 };
 // flight instead of paying one memory latency per 32 rows.
 template <typename T, int MODE, int U>
 __device__ __forceinline__ void reg_phase_u(const T *V, int64_t ld, int nc, int64_t rb, int64_t re, int64_t n,
-                                            const T *x, T *y, const T *coef, T (&acc)[RegCfg<T>::KP], T &ext) {
+                                            const T *x, T *y, const T *coef, T (&acc)[RegCfg<T>::KP], T &ext,
+                                            const CommArgs<T> *cm) {
     using C = RegCfg<T>;
     constexpr int R = C::R;
     constexpr int KU = C::KP / U;             // columns per part held per row group
@@ -143,6 +144,12 @@ __device__ __forceinline__ void reg_phase_u(const T *V, int64_t ld, int nc, int6
                 } else {
                     stcg16(y + r, yv);
                 }
+                if (MODE == kRegUpdateNorm && cm != nullptr) {
+                    // halo rows of w'' for the other ranks' next SpMV (P2P)
+                    for (int q = 0; q < cm->nranks; ++q)
+                        if (q != cm->rank && r >= cm->mir_lo[q] && r < cm->mir_hi[q])
+                            stcg16(cm->xg[q] + cm->row0 + r, yv);
+                }
             }
             if (MODE == kRegUpdateDots) {
 #pragma unroll
@@ -163,19 +170,24 @@ __device__ __forceinline__ void reg_phase_u(const T *V, int64_t ld, int nc, int6
 
 template <typename T, int MODE>
 __device__ __forceinline__ void reg_phase(const T *V, int64_t ld, int nc, int64_t rb, int64_t re, int64_t n,
-                                          const T *x, T *y, const T *coef, T (&acc)[RegCfg<T>::KP], T &ext) {
+                                          const T *x, T *y, const T *coef, T (&acc)[RegCfg<T>::KP], T &ext,
+                                          const CommArgs<T> *cm = nullptr) {
     using C = RegCfg<T>;
     const int ncp = (nc + C::P - 1) / C::P;   // columns per part
-    if (ncp * 8 <= C::KP) reg_phase_u<T, MODE, 8>(V, ld, nc, rb, re, n, x, y, coef, acc, ext);
-    else if (ncp * 4 <= C::KP) reg_phase_u<T, MODE, 4>(V, ld, nc, rb, re, n, x, y, coef, acc, ext);
-    else if (ncp * 2 <= C::KP) reg_phase_u<T, MODE, 2>(V, ld, nc, rb, re, n, x, y, coef, acc, ext);
-    else reg_phase_u<T, MODE, 1>(V, ld, nc, rb, re, n, x, y, coef, acc, ext);
+    if (ncp * 8 <= C::KP) reg_phase_u<T, MODE, 8>(V, ld, nc, rb, re, n, x, y, coef, acc, ext, cm);
+    else if (ncp * 4 <= C::KP) reg_phase_u<T, MODE, 4>(V, ld, nc, rb, re, n, x, y, coef, acc, ext, cm);
+    else if (ncp * 2 <= C::KP) reg_phase_u<T, MODE, 2>(V, ld, nc, rb, re, n, x, y, coef, acc, ext, cm);
+    else reg_phase_u<T, MODE, 1>(V, ld, nc, rb, re, n, x, y, coef, acc, ext, cm);
 }
 
 // CTA partials of the register layout: column c lives in part p = c % P,
 // slot i = c / P of the G lanes with that p in every warp.
+// `part` is this CTA's column of the local buffer (single GPU); with a comm,
+// the CTA's column rank * nb + cta of the phase's block in EVERY rank's
+// buffer is written (P2P stores; `off` = the phase block's element offset).
 template <typename T>
-__device__ __forceinline__ void reg_write_partials(T (&acc)[RegCfg<T>::KP], int nc, T extra, T *sm, T *part) {
+__device__ __forceinline__ void reg_write_partials(T (&acc)[RegCfg<T>::KP], int nc, T extra, T *sm, T *part,
+                                                   const CommArgs<T> *cm = nullptr, int64_t off = 0) {
     using C = RegCfg<T>;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane % C::G, p = lane / C::G;
@@ -194,7 +206,12 @@ __device__ __forceinline__ void reg_write_partials(T (&acc)[RegCfg<T>::KP], int 
         if (c < nc || c == kFExtra) {
             T s = sm[c];
             for (int w = 1; w < kFW; ++w) s += sm[w * kFSlots + c];
-            part[(int64_t)c * kFMaxCtas + blockIdx.x] = s;
+            if (cm == nullptr) {
+                part[(int64_t)c * kFMaxCtas + blockIdx.x] = s;
+            } else {
+                const int64_t col = (int64_t)cm->rank * gridDim.x + blockIdx.x;
+                for (int q = 0; q < cm->nranks; ++q) cm->part[q][off + (int64_t)c * kXStride + col] = s;
+            }
         }
     }
 }
@@ -233,9 +250,35 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
     const int64_t rpc = ((a.n + nb - 1) / nb + 63) / 64 * 64;   // rows per CTA, 64-aligned
     const int64_t rb = (int64_t)blockIdx.x * rpc;
     const int64_t re = (rb + rpc < a.n) ? rb + rpc : a.n;
-    T *partA = a.part, *partB = partA + (int64_t)kFSlots * kFMaxCtas,
-      *partC = partB + (int64_t)kFSlots * kFMaxCtas;
+    const bool multi = a.cm.nranks > 1;
+    const CommArgs<T> *cmp = multi ? &a.cm : nullptr;
+    // partials: single GPU -> local [slot][cta]; multi -> every rank's
+    // [phase][slot][rank * nb + cta], reduced over nranks * nb columns
+    const int64_t pblk = multi ? (int64_t)kFSlots * kXStride : (int64_t)kFSlots * kFMaxCtas;
+    T *pbase = multi ? a.cm.part[a.cm.rank] : a.part;
+    T *partA = pbase, *partB = pbase + pblk, *partC = pbase + 2 * pblk;
+    const unsigned ncol = multi ? nb * (unsigned)a.cm.nranks : nb;
+    const int pstride = multi ? kXStride : kFMaxCtas;
+    unsigned long long ep = multi ? __ldcg(a.cm.epoch) : 0ull;
     const bool lead = (blockIdx.x == 0);
+    // one grid barrier (all ranks when multi); true = a rank timed out
+    auto sync_all = [&]() -> bool {
+        if (!multi) {
+            grid_sync(a.bar, nb);
+            return false;
+        }
+        ++ep;
+        return grid_sync_x<T>(a.bar, nb, a.cm, ep);
+    };
+    auto finish = [&]() {
+        if (multi && lead && tid == 0) *a.cm.epoch = ep;
+    };
+#define MPK_SYNC_OR_ABORT()                        \
+    if (sync_all()) {                              \
+        if (lead && tid == 0) a.ctl->pad_ = 1;     \
+        finish();                                  \
+        return;                                    \
+    }
 
     if (tid == 0) {
         const T gamma = RN<T>::sqrt_(__ldcg(a.rnorm2));
@@ -253,16 +296,28 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
             a.ctl->steps = 0;
             a.ctl->breakdown = 0;
             a.ctl->tri_err = 0;
+            a.ctl->pad_ = 0;
             a.ctl->done = s_done;
             a.H.g[0] = gamma;
         }
     }
     __syncthreads();
+    if (multi) {
+        // v_0 = r0 / gamma reads halo rows of r0: stage r0 in the rank's
+        // global-length vector (the w'' slot) and mirror the boundary rows
+        for (int64_t r = rb + tid; r < re; r += kFB) {
+            const T v = a.r0[r];
+            a.wpp[r] = v;
+            for (int q = 0; q < a.cm.nranks; ++q)
+                if (q != a.cm.rank && r >= a.cm.mir_lo[q] && r < a.cm.mir_hi[q]) a.cm.xg[q][a.cm.row0 + r] = v;
+        }
+        MPK_SYNC_OR_ABORT();
+    }
 
     for (int k = 0; k < a.cap && !s_done; ++k) {
         const int nc = k + 1;
         MPK_MARK(12);
-        const T *src = (k == 0) ? a.r0 : a.wpp;
+        const T *src = (k == 0 && !multi) ? a.r0 : a.wpp;
         const T dv = (k == 0) ? s_gamma : s_beta;
         T *vk = a.V + (int64_t)k * a.ld;
         T acc[C::KP];
@@ -323,10 +378,10 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
         for (int i = 0; i < C::KP; ++i) acc[i] = T(0);
         reg_phase<T, kRegDots>(a.V, a.ld, nc, rb, re, a.n, a.w, nullptr, nullptr, acc, ext);
         MPK_MARK(2);
-        reg_write_partials<T>(acc, nc, an, sred, partA);
-        grid_sync(a.bar, nb);
+        reg_write_partials<T>(acc, nc, an, sred, partA, cmp, 0);
+        MPK_SYNC_OR_ABORT();
         MPK_MARK(3);
-        cross_reduce<T>(partA, nb, nc, nc + 1, sc1);   // sc1[0..k], sc1[nc] = ||w||^2
+        cross_reduce<T>(partA, ncol, nc, nc + 1, sc1, pstride);   // sc1[0..k], sc1[nc] = ||w||^2
         __syncthreads();
         MPK_MARK(4);
         // ---------------- phase B: w' = w - V c1 ; c2 = V^T w'
@@ -334,20 +389,20 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
         for (int i = 0; i < C::KP; ++i) acc[i] = T(0);
         reg_phase<T, kRegUpdateDots>(a.V, a.ld, nc, rb, re, a.n, a.w, a.wp, sc1, acc, ext);
         MPK_MARK(5);
-        reg_write_partials<T>(acc, nc, T(0), sred, partB);
-        grid_sync(a.bar, nb);
+        reg_write_partials<T>(acc, nc, T(0), sred, partB, cmp, pblk);
+        MPK_SYNC_OR_ABORT();
         MPK_MARK(6);
-        cross_reduce<T>(partB, nb, nc, nc, sc2);
+        cross_reduce<T>(partB, ncol, nc, nc, sc2, pstride);
         __syncthreads();
         MPK_MARK(7);
         // ---------------- phase C: w'' = w' - V c2 ; ||w''||^2
         T bn = T(0);
-        reg_phase<T, kRegUpdateNorm>(a.V, a.ld, nc, rb, re, a.n, a.wp, a.wpp, sc2, acc, bn);
+        reg_phase<T, kRegUpdateNorm>(a.V, a.ld, nc, rb, re, a.n, a.wp, a.wpp, sc2, acc, bn, cmp);
         MPK_MARK(8);
-        reg_write_partials<T>(acc, 0, bn, sred, partC);
-        grid_sync(a.bar, nb);
+        reg_write_partials<T>(acc, 0, bn, sred, partC, cmp, 2 * pblk);
+        MPK_SYNC_OR_ABORT();
         MPK_MARK(9);
-        cross_reduce<T>(partC, nb, 0, 1, &s_bn2);
+        cross_reduce<T>(partC, ncol, 0, 1, &s_bn2, pstride);
         __syncthreads();
         MPK_MARK(10);
         // ---------------- beta, append test, Givens (every CTA, identical)
@@ -366,6 +421,7 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
     T *sd = sc1;
     if (k > 0 && tid < 32) back_substitute<T>(a, k, ldr, sR, sg, sc2, sd, lead, s_app);
     __syncthreads();
+    finish();
     if (k > 0 && s_app) return;   // TriangularBreakdownError: x_out untouched
     if (lead) {
         for (int i = tid; i < k; i += kFB) a.H.d[i] = sd[i];
@@ -388,6 +444,7 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
     MPK_MARK(13);
     if (a.prof && tid < kProfSlots) g_fused_prof[blockIdx.x * kProfSlots + tid] = s_prof[tid];
 #undef MPK_MARK
+#undef MPK_SYNC_OR_ABORT
 }
 
 }  // namespace mpk
