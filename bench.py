@@ -9,8 +9,11 @@ A step = one full solve (b = ones, x0 = 0, m = 50, rtol 1e-10) with inputs
 resident in HBM (value); e2e repeats it through the public API with host
 (pinned) b/x0 and the solution copied back.  Working set (Krylov basis
 459 MB fp32 / 918 MB fp64) exceeds the 126 MB L2, so no explicit flush.
-N > 1: one independent replica per rank ("replicas only" for now; the
-row-partitioned solver is paper_2105_07544_b200.distributed), max over ranks.
+N > 1 (torchrun): the same system row-partitioned across the ranks
+(paper_2105_07544_b200.distributed: P2P halo stores and in-kernel cross-GPU
+reductions inside each rank's persistent cycle kernel), strong scaling, max
+over ranks.  MPK_SHARE_GPU=1 puts every rank on GPU 0 (gloo host
+collectives) to exercise the multi-process IPC path on a one-GPU box.
 """
 
 from __future__ import annotations
@@ -180,29 +183,62 @@ def main():
     import torch
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
+    share = os.environ.get("MPK_SHARE_GPU") == "1"   # test mode: N ranks on one GPU (gloo host collectives)
+    dev = 0 if share else local
+    torch.cuda.set_device(dev)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
     import paper_2105_07544_b200 as mk
     from paper_2105_07544_b200 import _lib
+    from paper_2105_07544_b200 import distributed as dd
 
     lib = _lib.load()
     P = mk.Precision
     preset, nx, desc = CONFIGS[args.config]
+    rule = "u" if args.config == "C4" else "n_u"   # n*u32 = 0.48 at 8M rows
     A = mk.generate_stencil(mk.ProblemSpec(preset, nx))
     A_low = mk.convert_matrix(A, P.binary32)
     n = A.n
-    inner = mk.SolverConfig(m=50, rtol=1e-4, precision=P.binary32, max_iters=100000)
+    inner = mk.SolverConfig(m=50, rtol=1e-4, precision=P.binary32, max_iters=100000, breakdown_rule=rule)
     icfg = mk.IrConfig(inner=inner, rtol=1e-10)
-    b_dev = torch.ones(n, dtype=torch.float64, device="cuda")
-    x0_dev = torch.zeros(n, dtype=torch.float64, device="cuda")
+    cfg64 = mk.SolverConfig(m=50, rtol=1e-10, max_iters=100000)
+    if world > 1:
+        comm = dd.TorchComm()
+        if share:
+            comm.ctas = max(1, int(lib.mpk_sm_count()) // world)
+        sysm = dd.LocalSystem(comm, A, A_low)
+        n_loc = sysm.n
+        b_dev = torch.ones(n_loc, dtype=torch.float64, device="cuda")
+        x0_dev = torch.zeros(n_loc, dtype=torch.float64, device="cuda")
+        solve_ir = lambda b, x0: dd.dist_gmres_ir(sysm, b, x0, icfg)  # noqa: E731
+        solve_64 = lambda b, x0: dd.dist_gmres_restarted(sysm, b, x0, cfg64)  # noqa: E731
+        wsi = sysm.workspace(50, P.binary32)
+    else:
+        from paper_2105_07544_b200.engine import CycleWorkspace
+
+        n_loc = n
+        b_dev = torch.ones(n, dtype=torch.float64, device="cuda")
+        x0_dev = torch.zeros(n, dtype=torch.float64, device="cuda")
+        solve_ir = lambda b, x0: mk.gmres_ir(A, b, x0, icfg, A_low=A_low)  # noqa: E731
+        solve_64 = lambda b, x0: mk.gmres_restarted(A, None, b, x0, cfg64)  # noqa: E731
+        wsi = CycleWorkspace.get(n, 50, P.binary32)
 
     def barrier():
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if world > 1:
+            got = [None] * world
+            torch.distributed.all_gather_object(got, float(v))
+            return max(got)
+        return v
 
     def timed(fn, steps):
         """CUDA-event time of `steps` back-to-back calls, max over ranks (ms)."""
@@ -212,25 +248,16 @@ def main():
         reps = [fn() for _ in range(steps)]
         ev1.record()
         barrier()
-        ms = ev0.elapsed_time(ev1)
-        if world > 1:
-            t = torch.tensor([ms], device="cuda")
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            ms = float(t.item())
-        return ms, reps
+        return max_over_ranks(ev0.elapsed_time(ev1)), reps
 
-    solve_ir = lambda: mk.gmres_ir(A, b_dev, x0_dev, icfg, A_low=A_low)  # noqa: E731
     for _ in range(args.warmup):
-        rep = solve_ir()
+        rep = solve_ir(b_dev, x0_dev)
     # timed region: K solves with per-kernel events on the launching stream
     launches0 = lib.mpk_launch_count()
     lib.mpk_prof_reset()
-    from paper_2105_07544_b200.engine import CycleWorkspace
-
-    wsi = CycleWorkspace.get(n, 50, P.binary32)
     wsi.flags = 1
-    with ClockSampler(local) as clk:
-        ms_ir, reps = timed(solve_ir, args.steps)
+    with ClockSampler(dev) as clk:
+        ms_ir, reps = timed(lambda: solve_ir(b_dev, x0_dev), args.steps)
     wsi.flags = 0
     launches = lib.mpk_launch_count() - launches0
     NC = 8
@@ -241,12 +268,13 @@ def main():
     lib.mpk_prof_read(pm, pc, pb, NC)
     rep = reps[-1]
     ms_step = ms_ir / args.steps
-    # algorithmic bytes of the inner cycles: per Arnoldi step at
-    # basis size j: SpMV + CGS2 sv*n*(4j+10); per cycle + correction sv*n*(k+2)
+    # algorithmic bytes of the inner cycles on this rank's rows:
+    # per Arnoldi step at basis size j: SpMV + CGS2 sv*n*(4j+10); per cycle
+    # the correction sv*n*(k+2)
     sv = 4
-    spmv_b = 2.0 * sv * n      # matrix-free stencil: x read + y write
+    spmv_b = 2.0 * sv * n_loc      # matrix-free stencil: x read + y write
     steps_per_cycle = cycle_steps(rep.history)
-    alg = sum(sum(spmv_b + sv * n * (4 * (k + 1) + 10) for k in range(st)) + sv * n * (st + 2)
+    alg = sum(sum(spmv_b + sv * n_loc * (4 * (k + 1) + 10) for k in range(st)) + sv * n_loc * (st + 2)
               for st in steps_per_cycle) * args.steps
     names = ["spmv+norm+dot1", "update1+dot2", "update2+norm+givens", "normalise", "precond",
              "correction", "residual", "persistent Arnoldi cycle (k_cycle_reg)"]
@@ -279,14 +307,16 @@ def main():
         "value": ms_step / 1e3,
         "unit": "s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-        "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": False, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
         "dtype": "f32-inner/f64-outer",
         "data": "synthetic (generated %s, b = ones, x0 = 0)" % preset,
-        "config": {"workload": "%s, GMRES-IR restart 50, rtol 1e-10, 1 B200 per rank" % desc,
-                   "config": args.config, "n": n, "nnz": A.nnz, "m": 50,
+        "config": {"workload": "%s, GMRES-IR restart 50, rtol 1e-10" % desc,
+                   "config": args.config, "n": n, "nnz": A.nnz, "m": 50, "breakdown_rule": rule,
                    "operator": "matrix-free stencil (bit-identical to CSR)",
-                   "parallelism": "replicas" if world > 1 else "single",
-                   "l2": "working set > L2 (basis %.0f MB)" % ((51 * n * 4) / 1e6)},
+                   "parallelism": ("row-partitioned x%d (P2P halo + in-kernel cross-GPU reductions)" % world
+                                   if world > 1 else "single"),
+                   "rows_per_rank": n_loc,
+                   "l2": "working set > L2 (basis %.0f MB per rank)" % ((51 * n_loc * 4) / 1e6)},
         "iters": rep.total_iters, "refinements": rep.restarts, "final_relres": rep.final_explicit_relres,
         "converged": bool(rep.converged),
         "ref_iters": REF_ITERS[args.config]["ir"],
@@ -304,22 +334,26 @@ def main():
                                           "per cycle: correction 4*n*(k+2) (SURVEY 8(d))"},
     }
     if not args.no_fp64:
-        cfg64 = mk.SolverConfig(m=50, rtol=1e-10, max_iters=100000)
-        solve64 = lambda: mk.gmres_restarted(A, None, b_dev, x0_dev, cfg64)  # noqa: E731
+        solve64 = lambda: solve_64(b_dev, x0_dev)  # noqa: E731
         solve64()
         ms64, reps64 = timed(solve64, 1)
         out["fp64_gmres_s"] = ms64 / 1e3
         out["fp64_iters"] = reps64[-1].total_iters
         out["ir_speedup_vs_fp64"] = (ms64 / 1e3) / (ms_step / 1e3)
     if not args.no_e2e:
-        bh = torch.ones(n, dtype=torch.float64).pin_memory()
-        xh = torch.zeros(n, dtype=torch.float64).pin_memory()
-        solve_e2e = lambda: mk.gmres_ir(A, bh, xh, icfg, A_low=A_low)  # noqa: E731
+        # public API with host (pinned) inputs; every step copies b and x0 in
+        # and the solution out (each rank its own rows when partitioned)
+        bh = torch.ones(n_loc, dtype=torch.float64).pin_memory()
+        xh = torch.zeros(n_loc, dtype=torch.float64).pin_memory()
+        if world > 1:
+            solve_e2e = lambda: dd.dist_gmres_ir(sysm, bh, xh, icfg).x.cpu()  # noqa: E731
+        else:
+            solve_e2e = lambda: mk.gmres_ir(A, bh, xh, icfg, A_low=A_low).x  # noqa: E731
         solve_e2e()
-        ms_e2e, reps_e = timed(solve_e2e, args.steps)
-        assert not reps_e[-1].x.is_cuda
+        ms_e2e, xs_e = timed(solve_e2e, args.steps)
+        assert not xs_e[-1].is_cuda
         out["e2e"] = {"value": ms_e2e / args.steps / 1e3, "unit": "s", "h2d_bytes_per_step": 2 * 8 * n,
-                      "d2h_bytes_per_step": 8 * n}
+                      "d2h_bytes_per_step": 8 * n, "note": "whole job: b and x0 in, x out (all ranks)"}
     out["clocks"] = clk.summary()
     if rank == 0 and world == 1 and not args.no_cpu:
         s_it, it, dt = cpu_sample(args.config, "ir", 50)
@@ -330,6 +364,7 @@ def main():
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
+        sysm.close()
         torch.distributed.destroy_process_group()
 
 

@@ -102,3 +102,30 @@ def test_random_nonsymmetric_far_columns(cuda, rng):
     assert rep.converged
     xs = np.linalg.solve(dense, b)
     assert np.abs(x - xs).max() <= 1e-8 * np.abs(xs).max()
+
+
+def test_two_processes_share_the_gpu_through_ipc(cuda, tmp_path):
+    """torchrun, 2 processes on GPU 0: CUDA-IPC peer pointers, system-scope
+    atomics across processes (time-sliced, hence a small problem)."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ, MPK_SHARE_GPU="1")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port),
+                          os.path.join(root, "tools", "dist_check.py"), "Laplace2D", "32"],
+                         capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = [ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1]
+    r = json.loads(line)
+    assert r["ir_converged"] and r["fp64_converged"] and r["ir_relres"] <= 1e-10
+    assert r["fp64_iters"] == r["single_fp64_iters"] == 71
+    assert abs(r["ir_iters"] - 150) <= 50
+    assert r["x_maxdiff"] <= 1e-8
