@@ -34,11 +34,12 @@ sys.path.insert(0, ROOT)
 CONFIGS = {
     "C1": ("Laplace3D", 40, "Laplace3D 7-point 40^3 (64k rows)"),
     "C2": ("BentPipe2D", 1500, "BentPipe2D convection-diffusion 1500^2 (2.25M rows)"),
+    "C3": ("UniFlow2D", 2500, "UniFlow2D convection-diffusion 2500^2 (6.25M rows)"),
     "C4": ("Laplace3D", 200, "Laplace3D 7-point 200^3 (8M rows)"),
 }
 # reference (mpkrylov) iteration counts on these configs (tests/golden/runs.json)
 REF_ITERS = {"C1": {"ir": 200, "fp64": 206}, "C2": {"ir": 10650, "fp64": 10833},
-             "C4": {"ir": None, "fp64": 4053}}
+             "C3": {"ir": None, "fp64": None}, "C4": {"ir": None, "fp64": 4053}}
 
 
 def peaks():
@@ -175,6 +176,7 @@ def main():
     ap.add_argument("--no-fp64", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--poly", type=int, default=0, help="GMRES-polynomial preconditioner degree (0: none)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -200,9 +202,21 @@ def main():
     lib = _lib.load()
     P = mk.Precision
     preset, nx, desc = CONFIGS[args.config]
-    rule = "u" if args.config == "C4" else "n_u"   # n*u32 = 0.48 at 8M rows
+    # the reference's beta <= n*u*||w|| test (n*u32 = 0.37 at 6.25M,
+    # 0.48 at 8M rows) declares false breakdowns on C3/C4; they run with "u"
+    rule = "u" if args.config in ("C3", "C4") else "n_u"
     A = mk.generate_stencil(mk.ProblemSpec(preset, nx))
     A_low = mk.convert_matrix(A, P.binary32)
+    M32 = M64 = None
+    if args.poly:
+        if world > 1:
+            raise SystemExit("the polynomial preconditioner runs on one GPU")
+        # setup outside the timed region (cli.py:166-168): fp32 polynomial for
+        # the IR inner cycles, fp64 polynomial for the fp64 GMRES comparison.
+        # NB on UniFlow2D the reference's poly (seed = ones) stalls GMRES
+        # (DESIGN.md 5), so C3's time-to-solution is quoted unpreconditioned
+        M32 = mk.build_gmres_poly(A_low, args.poly, np.ones(A.n, np.float32), rule=rule)
+        M64 = mk.build_gmres_poly(A, args.poly, np.ones(A.n))
     n = A.n
     inner = mk.SolverConfig(m=50, rtol=1e-4, precision=P.binary32, max_iters=100000, breakdown_rule=rule)
     icfg = mk.IrConfig(inner=inner, rtol=1e-10)
@@ -224,8 +238,8 @@ def main():
         n_loc = n
         b_dev = torch.ones(n, dtype=torch.float64, device="cuda")
         x0_dev = torch.zeros(n, dtype=torch.float64, device="cuda")
-        solve_ir = lambda b, x0: mk.gmres_ir(A, b, x0, icfg, A_low=A_low)  # noqa: E731
-        solve_64 = lambda b, x0: mk.gmres_restarted(A, None, b, x0, cfg64)  # noqa: E731
+        solve_ir = lambda b, x0: mk.gmres_ir(A, b, x0, icfg, M=M32, A_low=A_low)  # noqa: E731
+        solve_64 = lambda b, x0: mk.gmres_restarted(A, M64, b, x0, cfg64)  # noqa: E731
         wsi = CycleWorkspace.get(n, 50, P.binary32)
 
     def barrier():
@@ -348,14 +362,18 @@ def main():
         if world > 1:
             solve_e2e = lambda: dd.dist_gmres_ir(sysm, bh, xh, icfg).x.cpu()  # noqa: E731
         else:
-            solve_e2e = lambda: mk.gmres_ir(A, bh, xh, icfg, A_low=A_low).x  # noqa: E731
+            solve_e2e = lambda: mk.gmres_ir(A, bh, xh, icfg, M=M32, A_low=A_low).x  # noqa: E731
         solve_e2e()
         ms_e2e, xs_e = timed(solve_e2e, args.steps)
         assert not xs_e[-1].is_cuda
         out["e2e"] = {"value": ms_e2e / args.steps / 1e3, "unit": "s", "h2d_bytes_per_step": 2 * 8 * n,
                       "d2h_bytes_per_step": 8 * n, "note": "whole job: b and x0 in, x out (all ranks)"}
     out["clocks"] = clk.summary()
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if M32 is not None:
+        out["config"]["precond"] = {"kind": "gmres-poly", "degree_ir": M32.data.degree,
+                                    "degree_fp64": M64.data.degree, "seed": "ones"}
+        out["config"]["operator"] = "matrix-free stencil; poly apply = degree SpMVs per step"
+    if rank == 0 and world == 1 and not args.no_cpu and not args.poly:
         s_it, it, dt = cpu_sample(args.config, "ir", 50)
         full = REF_ITERS[args.config]["ir"] or rep.total_iters
         out["cpu_baseline"] = {"value": s_it * full, "unit": "s", "cores": cpu_cores(), "kind": "port",

@@ -597,13 +597,14 @@ def switch(A64, b, x0, switch_iter, m=50, rtol=1e-10, max_iters=100_000,
 # ---------------------------------------------------------------------------
 
 def synthetic_irregular(n, seed=20240817, mean_len=49, max_len=1000, band=2000,
-                        far_frac=0.01, dominance=1.1):
+                        far_frac=0.01, dominance=1.1, shift=1.0, signs="random"):
     """Config-5 matrix as specified in SURVEY §8(d) (calibrated far_frac default).
 
     Row length 1 + Geometric(1/mean_len) clipped to max_len; off-diagonal
     columns clip(i + U[-band, band]) or, with probability far_frac, U[0, n);
-    values N(0,1); duplicates summed by COO compression; diagonal =
-    dominance * sum|offdiag| + 1.  Returns (row_ptr, col_idx, values f64)."""
+    values N(0,1) (or -|N(0,1)| for signs="negative"); duplicates summed by
+    COO compression; diagonal = dominance * sum|offdiag| + shift.  Returns
+    (row_ptr, col_idx, values f64)."""
     rng = np.random.default_rng(seed)
     lens = np.minimum(1 + rng.geometric(1.0 / mean_len, size=n), max_len).astype(np.int64)
     off = lens - 1
@@ -613,12 +614,14 @@ def synthetic_irregular(n, seed=20240817, mean_len=49, max_len=1000, band=2000,
     far = rng.integers(0, n, size=tot)
     cols = np.where(rng.random(tot) < far_frac, far, near)
     vals = rng.standard_normal(tot)
+    if signs == "negative":
+        vals = -np.abs(vals)
     diag_mask = cols == rows
     rows, cols, vals = rows[~diag_mask], cols[~diag_mask], vals[~diag_mask]
     rp, ci, vv = coo_compress(rows, cols, vals, n)
     owner = np.repeat(np.arange(n, dtype=np.int64), np.diff(rp))
     rowsum = np.bincount(owner, weights=np.abs(vv), minlength=n)
-    diag = dominance * rowsum + 1.0
+    diag = dominance * rowsum + shift
     allr = np.concatenate([owner, np.arange(n, dtype=np.int64)])
     allc = np.concatenate([ci, np.arange(n, dtype=np.int64)])
     allv = np.concatenate([vv, diag])

@@ -602,7 +602,8 @@ int launch_fused_reg(const Op &op, const mpk_cycle_desc *d, int cap, double tf, 
     T *w = (T *)d->work;
     Ws ws = carve(d->ws);
     auto kern = k_cycle_reg<T, Op>;
-    const size_t smem = sizeof(T) * ((size_t)(m + 1) * m + 2 * m + (m + 1) + 2 * kFSlots + kFW * kFSlots);
+    const size_t smem =
+        sizeof(T) * ((size_t)(m + 1) * m + 2 * m + (m + 1) + 2 * kFSlots + kFW * kFSlots + kFW * kCsrWarpBuf);
     static size_t attr_set = 0;
     if (smem > attr_set) {
         cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -640,6 +641,10 @@ int launch_fused_reg(const Op &op, const mpk_cycle_desc *d, int cap, double tf, 
     fa.u = u;
     fa.final_col = (d->flags & 2) ? 1 : 0;
     fa.prof = (d->flags & 8) ? 1 : 0;
+    fa.diag = nullptr;
+    fa.z = w + 3 * d->ld;
+    if (d->M && d->M->kind == MPK_PC_JACOBI && d->M->block == 1 && d->M->dtype == d->dtype)
+        fa.diag = (const T *)d->M->lu;
     memset(&fa.cm, 0, sizeof(fa.cm));
     fa.cm.nranks = 1;
     if (d->nranks > 1) {
@@ -697,6 +702,17 @@ template <typename T> int run_cycle(const mpk_cycle_desc *d, cudaStream_t s) {
             (uintptr_t)d->work % 16 || (uintptr_t)d->r0 % 16)
             return fail(MPK_EUNSUPPORTED, "row-partitioned cycle: identity preconditioner, m <= 51, "
                                           "16-byte aligned buffers");
+        return with_op<T>(d->A, [&](auto op) -> int {
+            return launch_fused_reg<T, decltype(op)>(op, d, cap, tf, u, s);
+        });
+    }
+    // block Jacobi with 1x1 blocks is a diagonal scaling: the persistent
+    // register kernel applies it inside its SpMV input and correction
+    const bool diag1 = precond && d->M->kind == MPK_PC_JACOBI && d->M->block == 1 && d->M->n == n &&
+                       d->M->dtype == d->dtype;
+    if (diag1 && m + 1 <= kRegMaxCols && !(d->flags & 4) && !fused_use_tma() &&
+        (uintptr_t)d->x_out % 16 == 0 && (uintptr_t)d->V % 16 == 0 && (uintptr_t)d->work % 16 == 0 &&
+        (uintptr_t)d->r0 % 16 == 0 && (uintptr_t)d->M->lu % 16 == 0) {
         return with_op<T>(d->A, [&](auto op) -> int {
             return launch_fused_reg<T, decltype(op)>(op, d, cap, tf, u, s);
         });

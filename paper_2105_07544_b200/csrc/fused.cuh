@@ -78,6 +78,8 @@ template <typename T> struct FusedArgs {
     int final_col;    // collect_basis: also write V[:, steps] = w''/beta
     int prof;         // phase profiler on
     CommArgs<T> cm;   // nranks > 1: row-partitioned cycle
+    const T *diag;    // k_cycle_reg: diagonal right preconditioner a_ii (block Jacobi k = 1), or nullptr
+    T *z;             // k_cycle_reg: z = v_k / a_ii for the CTA's own rows
 };
 
 // Phase profiler (desc flag bit 3): per-CTA clock64 totals of each section,
@@ -423,13 +425,22 @@ __device__ __forceinline__ void back_substitute(const Args &a, int k, int ldr, c
 // CTA's own rows (written just before, one division per row) and divided on
 // the fly for halo rows owned by other CTAs (not yet written by them).  Own
 // rows go through L1 (this SM wrote them; neighbouring rows share lines).
+//
+// With a diagonal (block-Jacobi k = 1) right preconditioner the SpMV input is
+// z = M v_k = v_k / a_ii (lu_solve of a 1x1 block, preconditioners.py:133-139,
+// one IEEE division): own rows from the z slab, halo rows recomputed with the
+// same two roundings.
 template <typename T> struct XSlab {
     const T *src;
     const T *vk;
     T d;
     int64_t rb, re;
+    const T *diag = nullptr;   // a_ii (device), or identity
+    const T *z = nullptr;      // own rows of z = v_k / a_ii
     __device__ __forceinline__ T operator()(int64_t c) const {
-        return (c >= rb && c < re) ? vk[c] : RN<T>::div(__ldcg(src + c), d);
+        if (c >= rb && c < re) return diag ? z[c] : vk[c];
+        const T v = RN<T>::div(__ldcg(src + c), d);
+        return diag ? RN<T>::div(v, __ldg(diag + c)) : v;
     }
 };
 

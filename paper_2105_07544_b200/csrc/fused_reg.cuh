@@ -67,7 +67,7 @@ enum { kRegDots = 0, kRegUpdateDots = 1, kRegUpdateNorm = 2, kRegCorrect = 3 };
 template <typename T, int MODE, int U>
 __device__ __forceinline__ void reg_phase_u(const T *V, int64_t ld, int nc, int64_t rb, int64_t re, int64_t n,
                                             const T *x, T *y, const T *coef, T (&acc)[RegCfg<T>::KP], T &ext,
-                                            const CommArgs<T> *cm) {
+                                            const CommArgs<T> *cm, const T *diag) {
     using C = RegCfg<T>;
     constexpr int R = C::R;
     constexpr int KU = C::KP / U;             // columns per part held per row group
@@ -132,6 +132,12 @@ __device__ __forceinline__ void reg_phase_u(const T *V, int64_t ld, int nc, int6
 #pragma unroll
                 for (int e = 0; e < R; ++e) s[e] += __shfl_xor_sync(0xffffffffu, s[e], o);
             }
+            if (MODE == kRegCorrect && diag != nullptr && p == 0 && live) {
+                // x + M (V_k d) with M = diag^-1 (gmres.py:195-196)
+#pragma unroll
+                for (int e = 0; e < R; ++e)
+                    if (r + e < n) s[e] = RN<T>::div(s[e], __ldg(diag + r + e));
+            }
             Pack<T> yv;
 #pragma unroll
             for (int e = 0; e < R; ++e)
@@ -171,13 +177,13 @@ __device__ __forceinline__ void reg_phase_u(const T *V, int64_t ld, int nc, int6
 template <typename T, int MODE>
 __device__ __forceinline__ void reg_phase(const T *V, int64_t ld, int nc, int64_t rb, int64_t re, int64_t n,
                                           const T *x, T *y, const T *coef, T (&acc)[RegCfg<T>::KP], T &ext,
-                                          const CommArgs<T> *cm = nullptr) {
+                                          const CommArgs<T> *cm = nullptr, const T *diag = nullptr) {
     using C = RegCfg<T>;
     const int ncp = (nc + C::P - 1) / C::P;   // columns per part
-    if (ncp * 8 <= C::KP) reg_phase_u<T, MODE, 8>(V, ld, nc, rb, re, n, x, y, coef, acc, ext, cm);
-    else if (ncp * 4 <= C::KP) reg_phase_u<T, MODE, 4>(V, ld, nc, rb, re, n, x, y, coef, acc, ext, cm);
-    else if (ncp * 2 <= C::KP) reg_phase_u<T, MODE, 2>(V, ld, nc, rb, re, n, x, y, coef, acc, ext, cm);
-    else reg_phase_u<T, MODE, 1>(V, ld, nc, rb, re, n, x, y, coef, acc, ext, cm);
+    if (ncp * 8 <= C::KP) reg_phase_u<T, MODE, 8>(V, ld, nc, rb, re, n, x, y, coef, acc, ext, cm, diag);
+    else if (ncp * 4 <= C::KP) reg_phase_u<T, MODE, 4>(V, ld, nc, rb, re, n, x, y, coef, acc, ext, cm, diag);
+    else if (ncp * 2 <= C::KP) reg_phase_u<T, MODE, 2>(V, ld, nc, rb, re, n, x, y, coef, acc, ext, cm, diag);
+    else reg_phase_u<T, MODE, 1>(V, ld, nc, rb, re, n, x, y, coef, acc, ext, cm, diag);
 }
 
 // CTA partials of the register layout: column c lives in part p = c % P,
@@ -228,6 +234,7 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
     T *sc1 = sg + (m + 1);                     // kFSlots
     T *sc2 = sc1 + kFSlots;                    // kFSlots
     T *sred = sc2 + kFSlots;                   // kFW * kFSlots
+    T *sstage = sred + kFW * kFSlots;          // kFW * kCsrWarpBuf (CSR SpMV staging)
     __shared__ T s_gamma, s_beta, s_bn2;
     __shared__ int s_done, s_steps, s_break, s_app;
     __shared__ double s_scale;
@@ -339,6 +346,11 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
 #pragma unroll
                     for (int e = 0; e < R; ++e) q[u].v[e] = RN<T>::div(q[u].v[e], dv);
                     stcg16(vk + r + u * S, q[u]);
+                    if (a.diag) {
+#pragma unroll
+                        for (int e = 0; e < R; ++e) q[u].v[e] = RN<T>::div(q[u].v[e], __ldg(a.diag + r + u * S + e));
+                        stcg16(a.z + r + u * S, q[u]);
+                    }
                 }
             }
             for (; r < rv; r += S) {
@@ -346,15 +358,36 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
 #pragma unroll
                 for (int e = 0; e < R; ++e) q.v[e] = RN<T>::div(q.v[e], dv);
                 stcg16(vk + r, q);
+                if (a.diag) {
+#pragma unroll
+                    for (int e = 0; e < R; ++e) q.v[e] = RN<T>::div(q.v[e], __ldg(a.diag + r + e));
+                    stcg16(a.z + r, q);
+                }
             }
-            for (int64_t t = rv + tid; t < re; t += kFB) vk[t] = RN<T>::div(__ldcg(src + t), dv);
+            for (int64_t t = rv + tid; t < re; t += kFB) {
+                const T v = RN<T>::div(__ldcg(src + t), dv);
+                vk[t] = v;
+                if (a.diag) a.z[t] = RN<T>::div(v, __ldg(a.diag + t));
+            }
         }
         MPK_MARK(0);
         __syncthreads();
-        {
+        if constexpr (!Op::kStencil) {
+            // CSR: warp-cooperative 32-row groups (coalesced entries, row-sequential sums)
+            const XSlab<T> xs{src, vk, dv, rb, re, a.diag, a.z};
+            const int lane = tid & 31, warp = tid >> 5;
+            T *sb = sstage + warp * kCsrWarpBuf;
+            for (int64_t r0 = rb + (int64_t)warp * 32; r0 < re; r0 += (int64_t)kFW * 32) {
+                const T wr = A.warp_rows(r0, re, xs, sb);
+                if (r0 + lane < re) {
+                    a.w[r0 + lane] = wr;
+                    an += wr * wr;
+                }
+            }
+        } else {
             // w = A v_k, eight rows per thread per trip
             constexpr int UR = 8;
-            const XSlab<T> xs{src, vk, dv, rb, re};
+            const XSlab<T> xs{src, vk, dv, rb, re, a.diag, a.z};
             int64_t r = rb + tid;
             for (; r + (UR - 1) * kFB < re; r += UR * kFB) {
                 T wv[UR];
@@ -439,7 +472,7 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
     {
         T acc[C::KP];
         T ext = T(0);
-        reg_phase<T, kRegCorrect>(a.V, a.ld, k, rb, re, a.n, a.x0, a.x_out, sd, acc, ext);
+        reg_phase<T, kRegCorrect>(a.V, a.ld, k, rb, re, a.n, a.x0, a.x_out, sd, acc, ext, nullptr, a.diag);
     }
     MPK_MARK(13);
     if (a.prof && tid < kProfSlots) g_fused_prof[blockIdx.x * kProfSlots + tid] = s_prof[tid];

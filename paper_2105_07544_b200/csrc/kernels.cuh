@@ -51,6 +51,24 @@ __device__ __forceinline__ bool skip(const int32_t *done) {
 __device__ __forceinline__ int64_t gtid() { return (int64_t)blockIdx.x * blockDim.x + threadIdx.x; }
 __device__ __forceinline__ int64_t gstride() { return (int64_t)gridDim.x * blockDim.x; }
 
+// Row loop of an SpMV-carrying kernel.  Stencils: thread per row, grid-
+// strided.  CSR: 32-row groups per warp, grid-strided over groups, each
+// evaluated by CsrOp::warp_rows (coalesced entry loads, bit-identical sums);
+// fn(r, y_r) runs on the lane owning row r.  `sb` is the warp's staging.
+template <typename T, class Op, class X, class F>
+__device__ __forceinline__ void for_rows(const Op &A, X x, T *sb, F &&fn) {
+    if constexpr (Op::kStencil) {
+        for (int64_t r = gtid(); r < A.n; r += gstride()) fn(r, A.row(r, x));
+    } else {
+        const int lane = threadIdx.x & 31;
+        const int64_t gw = gtid() >> 5, nw = gstride() >> 5;
+        for (int64_t r0 = gw * 32; r0 < A.n; r0 += nw * 32) {
+            const T y = A.warp_rows(r0, A.n, x, sb);
+            if (r0 + lane < A.n) fn(r0 + lane, y);
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // P1: (normalise) + SpMV + ||w||^2 + first projection V^T w
 // ---------------------------------------------------------------------------
@@ -67,14 +85,13 @@ __global__ void __launch_bounds__(kBlock) k_spmv_dot(Op A, const T *__restrict__
 #pragma unroll
     for (int c = 0; c < NC; ++c) acc[c] = T(0);
     T an = T(0);
-    for (int64_t r = gtid(); r < A.n; r += gstride()) {
-        T wr, own = T(0);
+    __shared__ T sbuf[Op::kStencil ? 1 : (kBlock / 32) * kCsrWarpBuf];
+    T *sb = sbuf + (Op::kStencil ? 0 : (threadIdx.x >> 5) * kCsrWarpBuf);
+    auto body = [&](int64_t r, T wr) {
+        T own = T(0);
         if constexpr (NORM) {
-            wr = A.row(r, XScaled<T>{src, dv});
             own = RN<T>::div(src[r], dv);
             vcol[r] = own;
-        } else {
-            wr = A.row(r, XPlain<T>{src});
         }
         w[r] = wr;
         an += wr * wr;
@@ -85,6 +102,11 @@ __global__ void __launch_bounds__(kBlock) k_spmv_dot(Op A, const T *__restrict__
                 acc[c] += v * wr;
             }
         }
+    };
+    if constexpr (NORM) {
+        for_rows<T>(A, XScaled<T>{src, dv}, sb, body);
+    } else {
+        for_rows<T>(A, XPlain<T>{src}, sb, body);
     }
     block_reduce_cols<T, NC>(acc, ndot, an, sm, partials + (int64_t)blockIdx.x * kStride);
     if (last_cta(counter)) {
@@ -431,8 +453,10 @@ __global__ void __launch_bounds__(kBlock) k_residual(Op A, const T *__restrict__
     __shared__ float smf[(kBlock / 32) * 2];
     T an = T(0);
     float al = 0.f;
-    for (int64_t i = gtid(); i < A.n; i += gstride()) {
-        const T ri = RN<T>::sub(b[i], A.row(i, XPlain<T>{x}));
+    __shared__ T sbuf[Op::kStencil ? 1 : (kBlock / 32) * kCsrWarpBuf];
+    T *sb = sbuf + (Op::kStencil ? 0 : (threadIdx.x >> 5) * kCsrWarpBuf);
+    for_rows<T>(A, XPlain<T>{x}, sb, [&](int64_t i, T ax) {
+        const T ri = RN<T>::sub(b[i], ax);
         if (r) r[i] = ri;
         an += ri * ri;
         if constexpr (LOW) {
@@ -440,7 +464,7 @@ __global__ void __launch_bounds__(kBlock) k_residual(Op A, const T *__restrict__
             rlow[i] = li;
             al += li * li;
         }
-    }
+    });
     T d1[1] = {T(0)};
     block_reduce_cols<T, 1>(d1, 0, an, sm, partials + (int64_t)blockIdx.x * kStride);
     if constexpr (LOW) {
@@ -472,7 +496,9 @@ __global__ void k_ir_update(int64_t n, double *__restrict__ x, const float *__re
 // ---------------------------------------------------------------------------
 template <typename T, class Op>
 __global__ void __launch_bounds__(kBlock) k_spmv(Op A, const T *__restrict__ x, T *__restrict__ y) {
-    for (int64_t r = gtid(); r < A.n; r += gstride()) y[r] = A.row(r, XPlain<T>{x});
+    __shared__ T sbuf[Op::kStencil ? 1 : (kBlock / 32) * kCsrWarpBuf];
+    T *sb = sbuf + (Op::kStencil ? 0 : (threadIdx.x >> 5) * kCsrWarpBuf);
+    for_rows<T>(A, XPlain<T>{x}, sb, [&](int64_t r, T yr) { y[r] = yr; });
 }
 
 template <typename S, typename D>

@@ -15,6 +15,12 @@
 
 namespace mpk {
 
+// Products staged per warp for the warp-cooperative CSR rows (elements of T):
+// 8 entries per lane per chunk (16 measured 10% faster on the ~50-entry rows
+// of config 5 in fp32 but 25-35% slower on 5-7-entry stencil rows).
+template <typename T> struct CsrStage { static constexpr int value = 8; };
+constexpr int kCsrWarpBuf = 256;               // staging elements per warp
+
 template <typename T> struct CsrOp {
     int64_t n;
     const int32_t *__restrict__ rp;
@@ -26,6 +32,66 @@ template <typename T> struct CsrOp {
         T acc = T(0);
         for (int32_t p = p0; p < p1; ++p)
             acc = RN<T>::add(acc, RN<T>::mul(__ldg(v + p), x((int64_t)__ldg(ci + p))));
+        return acc;
+    }
+
+    // Rows [r0, min(r0 + 32, rend)) by one full warp, lane i owning row
+    // r0 + i: the warp walks the rows' contiguous entry range in chunks of
+    // 32 x kCsrStage, every lane loading consecutive entries (coalesced
+    // values / column indices) and staging the rounded products value*x[col]
+    // in shared memory in storage order; each lane then adds its own row's
+    // products left to right.  Same roundings in the same order as
+    // csr_matvec (sparse.py:190-206), so bit-identical to row(), at
+    // coalesced-load speed for long, irregular rows.  `sb`: kCsrWarpBuf
+    // elements of this warp.  Returns the lane's row value (0 past rend).
+    template <class X> __device__ __forceinline__ T warp_rows(int64_t r0, int64_t rend, X x, T *sb) const {
+        constexpr int kCsrStage = CsrStage<T>::value;
+        constexpr int kChunk = 32 * kCsrStage;
+        const int lane = threadIdx.x & 31;
+        const int64_t last = (r0 + 32 < rend ? r0 + 32 : rend) - 1;
+        const bool mine = r0 + lane <= last;
+        int32_t ps = 0, pe = 0;
+        if (mine) {
+            ps = __ldg(rp + r0 + lane);
+            pe = __ldg(rp + r0 + lane + 1);
+        }
+        const int32_t base = __ldg(rp + r0), end = __ldg(rp + last + 1);
+        T acc = T(0);
+        int32_t p = ps;
+        // software pipeline: the next chunk's values / column indices are in
+        // flight while this chunk's x entries are gathered
+        T va[kCsrStage];
+        int32_t ca[kCsrStage];
+#pragma unroll
+        for (int j = 0; j < kCsrStage; ++j) {
+            const int32_t e = base + j * 32 + lane;
+            va[j] = (e < end) ? __ldg(v + e) : T(0);
+            ca[j] = (e < end) ? __ldg(ci + e) : -1;
+        }
+        for (int32_t cb = base; cb < end; cb += kChunk) {
+            T xs[kCsrStage];
+#pragma unroll
+            for (int j = 0; j < kCsrStage; ++j) xs[j] = (ca[j] >= 0) ? x((int64_t)ca[j]) : T(0);
+            T vn[kCsrStage];
+            int32_t cn[kCsrStage];
+#pragma unroll
+            for (int j = 0; j < kCsrStage; ++j) {
+                const int32_t e = cb + kChunk + j * 32 + lane;
+                vn[j] = (e < end) ? __ldg(v + e) : T(0);
+                cn[j] = (e < end) ? __ldg(ci + e) : -1;
+            }
+#pragma unroll
+            for (int j = 0; j < kCsrStage; ++j) sb[j * 32 + lane] = RN<T>::mul(va[j], xs[j]);
+            __syncwarp();
+            const int32_t ce = (cb + kChunk < pe) ? cb + kChunk : pe;
+            for (; p < ce; ++p) acc = RN<T>::add(acc, sb[p - cb]);
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < kCsrStage; ++j) {
+                va[j] = vn[j];
+                ca[j] = cn[j];
+            }
+        }
         return acc;
     }
     static constexpr bool kStencil = false;
@@ -114,6 +180,11 @@ template <typename T> struct StencilOp {
         if (ix < nx - 1) acc = RN<T>::add(acc, RN<T>::mul(c3, x(r + 1)));
         if (iy < nx - 1) acc = RN<T>::add(acc, RN<T>::mul(c4, x(r + nx)));
         return acc;
+    }
+    // lane-per-row over [r0, r0 + 32) (interface of CsrOp::warp_rows)
+    template <class X> __device__ __forceinline__ T warp_rows(int64_t r0, int64_t rend, X x, T *) const {
+        const int64_t r = r0 + (threadIdx.x & 31);
+        return r < rend ? row(r, x) : T(0);
     }
     static constexpr bool kStencil = true;
 };

@@ -115,3 +115,36 @@ def test_preconditioned_goldens(cuda, runs):
     M32 = mk.build_gmres_poly(mk.convert_matrix(st, P.binary32), 20, np.ones(st.n, np.float32))
     rep = mk.gmres_ir(st, np.ones(st.n), np.zeros(st.n), mk.IrConfig(inner=inner, rtol=1e-10), M=M32)
     assert rep.converged and abs(rep.total_iters - runs["ir_poly20_st32"]["iters"]) <= 50
+
+
+def test_jacobi1_fused_cycle_matches_multikernel_and_oracle(cuda):
+    """Block Jacobi k=1 runs inside the persistent cycle kernel (diagonal
+    scaling of the SpMV input and of the correction); same iteration counts
+    as the multi-kernel path and within one cycle of the oracle."""
+    from oracle import mpk_oracle as O
+    from paper_2105_07544_b200.engine import CycleWorkspace
+
+    A = mk.synthetic_irregular(12000, band=300, signs="negative", dominance=1.01, shift=1e-3)
+    b = np.ones(A.n)
+    J = mk.build_block_jacobi(A, 1)
+    cfg = mk.SolverConfig(m=50, rtol=1e-10, max_iters=5000)
+    fused = mk.gmres_restarted(A, J, b, np.zeros(A.n), cfg)
+    ws = CycleWorkspace.get(A.n, 50, P.binary64)
+    ws.flags = 4
+    try:
+        multi = mk.gmres_restarted(A, J, b, np.zeros(A.n), cfg)
+    finally:
+        ws.flags = 0
+    assert fused.converged and multi.converged
+    assert abs(fused.total_iters - multi.total_iters) <= 2
+    ref = O.restarted((A.row_ptr, A.col_idx, A.values), O.jacobi_build(A.row_ptr, A.col_idx, A.values, 1,
+                                                                         np.float64),
+                      b, np.zeros(A.n), 50, 1e-10, 5000)
+    assert ref.converged and abs(fused.total_iters - ref.iters) <= 50
+    assert np.abs(fused.x - ref.x).max() <= 1e-7 * np.abs(ref.x).max()
+    # GMRES-IR with the fp32 diagonal
+    Al = mk.convert_matrix(A, P.binary32)
+    J32 = mk.build_block_jacobi(Al, 1)
+    inner = mk.SolverConfig(m=50, rtol=1e-4, precision=P.binary32, max_iters=5000)
+    ir = mk.gmres_ir(A, b, np.zeros(A.n), mk.IrConfig(inner=inner, rtol=1e-10), M=J32, A_low=Al)
+    assert ir.converged and ir.final_explicit_relres <= 1e-10
