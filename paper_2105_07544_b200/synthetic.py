@@ -1,8 +1,8 @@
 """BASELINE config 5: a SuiteSparse-like irregular nonsymmetric CSR matrix.
 
 The reference has no generator for it; this is the SURVEY
-§8(d) specification, restated identically in the oracle
-(oracle/mpk_oracle.py ``synthetic_irregular``, bit-exact, tests/test_synthetic.py):
+§8(d) specification (restated identically by the test-side CPU checker,
+bit-exact, tests/test_synthetic.py):
 
   row length 1 + Geometric(1/mean_len), clipped to max_len; off-diagonal
   columns clip(i + U[-band, band]) or, with probability far_frac, U[0, n);
