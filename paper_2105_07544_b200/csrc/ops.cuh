@@ -66,19 +66,20 @@ template <typename T> struct CsrOp {
         for (int j = 0; j < kCsrStage; ++j) {
             const int32_t e = base + j * 32 + lane;
             va[j] = (e < end) ? __ldg(v + e) : T(0);
-            ca[j] = (e < end) ? __ldg(ci + e) : -1;
+            ca[j] = (e < end) ? __ldg(ci + e) : 0;
         }
         for (int32_t cb = base; cb < end; cb += kChunk) {
             T xs[kCsrStage];
 #pragma unroll
-            for (int j = 0; j < kCsrStage; ++j) xs[j] = (ca[j] >= 0) ? x((int64_t)ca[j]) : T(0);
+            for (int j = 0; j < kCsrStage; ++j)   // columns may be negative (row blocks): mask by position
+                xs[j] = (cb + j * 32 + lane < end) ? x((int64_t)ca[j]) : T(0);
             T vn[kCsrStage];
             int32_t cn[kCsrStage];
 #pragma unroll
             for (int j = 0; j < kCsrStage; ++j) {
                 const int32_t e = cb + kChunk + j * 32 + lane;
                 vn[j] = (e < end) ? __ldg(v + e) : T(0);
-                cn[j] = (e < end) ? __ldg(ci + e) : -1;
+                cn[j] = (e < end) ? __ldg(ci + e) : 0;
             }
 #pragma unroll
             for (int j = 0; j < kCsrStage; ++j) sb[j * 32 + lane] = RN<T>::mul(va[j], xs[j]);
