@@ -39,6 +39,27 @@ template <> struct RN<float> {
 
 template <typename T> __device__ __forceinline__ T ldcg(const T *p) { return __ldcg(p); }
 
+// 16-byte row groups (4 fp32 / 2 fp64 consecutive rows)
+template <typename T> struct alignas(16) Pack {
+    T v[16 / sizeof(T)];
+};
+
+__device__ __forceinline__ Pack<float> ldcg16(const float *p) {
+    const float4 q = __ldcg(reinterpret_cast<const float4 *>(p));
+    return Pack<float>{{q.x, q.y, q.z, q.w}};
+}
+__device__ __forceinline__ Pack<double> ldcg16(const double *p) {
+    const double2 q = __ldcg(reinterpret_cast<const double2 *>(p));
+    return Pack<double>{{q.x, q.y}};
+}
+__device__ __forceinline__ void stcg16(float *p, const Pack<float> &v) {
+    __stcg(reinterpret_cast<float4 *>(p), make_float4(v.v[0], v.v[1], v.v[2], v.v[3]));
+}
+__device__ __forceinline__ void stcg16(double *p, const Pack<double> &v) {
+    __stcg(reinterpret_cast<double2 *>(p), make_double2(v.v[0], v.v[1]));
+}
+
+
 // Warp-level sum (fixed butterfly order -> deterministic).
 template <typename T> __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

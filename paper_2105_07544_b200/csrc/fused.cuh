@@ -442,6 +442,20 @@ template <typename T> struct XSlab {
         const T v = RN<T>::div(__ldcg(src + c), d);
         return diag ? RN<T>::div(v, __ldg(diag + c)) : v;
     }
+    // 16-byte group starting at c (c and the CTA bounds are group-aligned,
+    // so the whole group is own or halo)
+    __device__ __forceinline__ Pack<T> vec(int64_t c) const {
+        const bool own = c >= rb && c < re;
+        Pack<T> q = ldcg16((own ? (diag ? z : vk) : src) + c);
+        if (!own) {
+#pragma unroll
+            for (int e = 0; e < (int)(16 / sizeof(T)); ++e) {
+                q.v[e] = RN<T>::div(q.v[e], d);
+                if (diag) q.v[e] = RN<T>::div(q.v[e], __ldg(diag + c + e));
+            }
+        }
+        return q;
+    }
 };
 
 template <typename T, class Op, int TR>

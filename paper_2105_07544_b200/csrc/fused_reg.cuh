@@ -34,25 +34,6 @@ template <typename T> struct RegCfg {
     static constexpr int WR = G * R;                   // rows per warp trip
 };
 
-template <typename T> struct alignas(16) Pack {
-    T v[16 / sizeof(T)];
-};
-
-__device__ __forceinline__ Pack<float> ldcg16(const float *p) {
-    const float4 q = __ldcg(reinterpret_cast<const float4 *>(p));
-    return Pack<float>{{q.x, q.y, q.z, q.w}};
-}
-__device__ __forceinline__ Pack<double> ldcg16(const double *p) {
-    const double2 q = __ldcg(reinterpret_cast<const double2 *>(p));
-    return Pack<double>{{q.x, q.y}};
-}
-__device__ __forceinline__ void stcg16(float *p, const Pack<float> &v) {
-    __stcg(reinterpret_cast<float4 *>(p), make_float4(v.v[0], v.v[1], v.v[2], v.v[3]));
-}
-__device__ __forceinline__ void stcg16(double *p, const Pack<double> &v) {
-    __stcg(reinterpret_cast<double2 *>(p), make_double2(v.v[0], v.v[1]));
-}
-
 enum { kRegDots = 0, kRegUpdateDots = 1, kRegUpdateNorm = 2, kRegCorrect = 3 };
 
 // One streaming pass over the CTA's rows [rb, re) (n = global length for the
@@ -222,6 +203,60 @@ __device__ __forceinline__ void reg_write_partials(T (&acc)[RegCfg<T>::KP], int 
     }
 }
 
+// Phase A's SpMV w = A v_k over the CTA's rows, returns the thread's part of
+// ||w||^2.  Out of line (noinline) so its register needs (BentPipe
+// coefficient arithmetic, the CSR staging) do not raise register pressure in
+// the streaming phases, which are kept spill-free.
+template <typename T, class Op>
+__device__ __noinline__ T phase_a_spmv(const Op &A, const XSlab<T> xs, T *w, int64_t rb, int64_t re, T *sstage) {
+    T an = T(0);
+    if constexpr (!Op::kStencil) {
+        // CSR: warp-cooperative 32-row groups (coalesced entries, row-sequential sums)
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        T *sb = sstage + warp * kCsrWarpBuf;
+        for (int64_t r0 = rb + (int64_t)warp * 32; r0 < re; r0 += (int64_t)kFW * 32) {
+            const T wr = A.warp_rows(r0, re, xs, sb);
+            if (r0 + lane < re) {
+                w[r0 + lane] = wr;
+                an += wr * wr;
+            }
+        }
+    } else if (A.group_ok()) {
+        // 16-byte row groups: vector reads of the group and its S/N (B/U)
+        // neighbours, one group per thread per trip
+        constexpr int R = RegCfg<T>::R;
+        auto xv = [&](int64_t c) { return xs.vec(c); };
+        constexpr int64_t S = (int64_t)kFB * R;
+        for (int64_t r = rb + (int64_t)threadIdx.x * R; r < re; r += S) {
+            Pack<T> o;
+            A.row_group(r, xv, xs, o.v);
+            stcg16(w + r, o);
+#pragma unroll
+            for (int e = 0; e < R; ++e) an += o.v[e] * o.v[e];
+        }
+    } else {
+        // eight rows per thread per trip
+        constexpr int UR = 8;
+        int64_t r = rb + threadIdx.x;
+        for (; r + (UR - 1) * kFB < re; r += UR * kFB) {
+            T wv[UR];
+#pragma unroll
+            for (int u = 0; u < UR; ++u) wv[u] = A.row(r + u * kFB, xs);
+#pragma unroll
+            for (int u = 0; u < UR; ++u) {
+                w[r + u * kFB] = wv[u];
+                an += wv[u] * wv[u];
+            }
+        }
+        for (; r < re; r += kFB) {
+            const T wr = A.row(r, xs);
+            w[r] = wr;
+            an += wr * wr;
+        }
+    }
+    return an;
+}
+
 template <typename T, class Op>
 __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
     using C = RegCfg<T>;
@@ -372,39 +407,7 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
         }
         MPK_MARK(0);
         __syncthreads();
-        if constexpr (!Op::kStencil) {
-            // CSR: warp-cooperative 32-row groups (coalesced entries, row-sequential sums)
-            const XSlab<T> xs{src, vk, dv, rb, re, a.diag, a.z};
-            const int lane = tid & 31, warp = tid >> 5;
-            T *sb = sstage + warp * kCsrWarpBuf;
-            for (int64_t r0 = rb + (int64_t)warp * 32; r0 < re; r0 += (int64_t)kFW * 32) {
-                const T wr = A.warp_rows(r0, re, xs, sb);
-                if (r0 + lane < re) {
-                    a.w[r0 + lane] = wr;
-                    an += wr * wr;
-                }
-            }
-        } else {
-            // w = A v_k, eight rows per thread per trip
-            constexpr int UR = 8;
-            const XSlab<T> xs{src, vk, dv, rb, re, a.diag, a.z};
-            int64_t r = rb + tid;
-            for (; r + (UR - 1) * kFB < re; r += UR * kFB) {
-                T wv[UR];
-#pragma unroll
-                for (int u = 0; u < UR; ++u) wv[u] = A.row(r + u * kFB, xs);
-#pragma unroll
-                for (int u = 0; u < UR; ++u) {
-                    a.w[r + u * kFB] = wv[u];
-                    an += wv[u] * wv[u];
-                }
-            }
-            for (; r < re; r += kFB) {
-                const T wr = A.row(r, xs);
-                a.w[r] = wr;
-                an += wr * wr;
-            }
-        }
+        an = phase_a_spmv<T>(A, XSlab<T>{src, vk, dv, rb, re, a.diag, a.z}, a.w, rb, re, sstage);
         MPK_MARK(1);
         __syncthreads();   // w rows of this CTA visible to the other lanes' 16-byte loads
 #pragma unroll

@@ -182,6 +182,83 @@ template <typename T> struct StencilOp {
         if (iy < nx - 1) acc = RN<T>::add(acc, RN<T>::mul(c4, x(r + nx)));
         return acc;
     }
+    // Rows [r, r + R) of one grid line (R = 16 / sizeof(T); needs r % R == 0
+    // and group_ok()): the S/N (and B/U) neighbours and the rows themselves
+    // are R-wide vector reads (xv), the W of the first and the E of the last
+    // row two scalar reads (xs); every row's products are added in the
+    // reference's displacement order, so out[] equals row(r + e).
+    static constexpr int R = 16 / (int)sizeof(T);
+    __device__ __forceinline__ bool group_ok() const {
+        return k.preset != MPK_STRETCHED2D && k.nx % R == 0 && k.row0 % R == 0;
+    }
+    template <class XV, class XS>
+    __device__ __forceinline__ void row_group(int64_t r, XV xv, XS xs, T (&out)[R]) const {
+        const uint32_t g = (uint32_t)(k.row0 + r);
+        const int nx = k.nx;
+        const uint32_t q1 = k.dnx.div(g);
+        const int ix0 = (int)(g - q1 * (uint32_t)nx);
+        const Pack<T> c = xv(r);
+        const T xw = (ix0 > 0) ? xs(r - 1) : T(0);
+        const T xe = (ix0 + R - 1 < nx - 1) ? xs(r + R) : T(0);
+        if (k.preset == MPK_LAPLACE3D) {
+            const int64_t nxy = (int64_t)nx * nx;
+            const uint32_t iz_ = k.dnxy.div(g);
+            const int iy = (int)(q1 - iz_ * (uint32_t)nx), iz = (int)iz_;
+            const bool B = iz > 0, S = iy > 0, N = iy < nx - 1, U = iz < nx - 1;
+            Pack<T> pb, ps, pn, pu;
+            if (B) pb = xv(r - nxy);
+            if (S) ps = xv(r - nx);
+            if (N) pn = xv(r + nx);
+            if (U) pu = xv(r + nxy);
+#pragma unroll
+            for (int e = 0; e < R; ++e) {
+                const int ix = ix0 + e;
+                T acc = T(0);
+                if (B) acc = RN<T>::add(acc, RN<T>::mul(cT[0], pb.v[e]));
+                if (S) acc = RN<T>::add(acc, RN<T>::mul(cT[1], ps.v[e]));
+                if (ix > 0) acc = RN<T>::add(acc, RN<T>::mul(cT[2], e ? c.v[e ? e - 1 : 0] : xw));
+                acc = RN<T>::add(acc, RN<T>::mul(cT[3], c.v[e]));
+                if (ix < nx - 1) acc = RN<T>::add(acc, RN<T>::mul(cT[4], e < R - 1 ? c.v[e < R - 1 ? e + 1 : 0] : xe));
+                if (N) acc = RN<T>::add(acc, RN<T>::mul(cT[5], pn.v[e]));
+                if (U) acc = RN<T>::add(acc, RN<T>::mul(cT[6], pu.v[e]));
+                out[e] = acc;
+            }
+            return;
+        }
+        const int iy = (int)q1;
+        const bool S = iy > 0, N = iy < nx - 1;
+        Pack<T> ps, pn;
+        if (S) ps = xv(r - nx);
+        if (N) pn = xv(r + nx);
+        double pyc = 0.0, py1 = 0.0;
+        if (k.preset == MPK_BENTPIPE2D) {
+            const double py = __dmul_rn((double)(iy + 1), k.h);
+            pyc = __dmul_rn(k.cc2, py);                      // (c*2.0)*py
+            py1 = __dsub_rn(1.0, __dmul_rn(py, py));         // 1 - py*py
+        }
+#pragma unroll
+        for (int e = 0; e < R; ++e) {
+            const int ix = ix0 + e;
+            T c0 = cT[0], c1 = cT[1], c2 = cT[2], c3 = cT[3], c4 = cT[4];
+            if (k.preset == MPK_BENTPIPE2D) {
+                // stencils.py:104-115, same operations and order as row()
+                const double px = __dmul_rn((double)(ix + 1), k.h);
+                const double ux = __dmul_rn(pyc, __dsub_rn(1.0, __dmul_rn(px, px)));
+                const double uy = __dmul_rn(__dmul_rn(k.ncc2, px), py1);
+                c0 = RN<T>::from_double(__dsub_rn(-1.0, __dmul_rn(k.hh, uy)));
+                c1 = RN<T>::from_double(__dsub_rn(-1.0, __dmul_rn(k.hh, ux)));
+                c3 = RN<T>::from_double(__dadd_rn(-1.0, __dmul_rn(k.hh, ux)));
+                c4 = RN<T>::from_double(__dadd_rn(-1.0, __dmul_rn(k.hh, uy)));
+            }
+            T acc = T(0);
+            if (S) acc = RN<T>::add(acc, RN<T>::mul(c0, ps.v[e]));
+            if (ix > 0) acc = RN<T>::add(acc, RN<T>::mul(c1, e ? c.v[e ? e - 1 : 0] : xw));
+            acc = RN<T>::add(acc, RN<T>::mul(c2, c.v[e]));
+            if (ix < nx - 1) acc = RN<T>::add(acc, RN<T>::mul(c3, e < R - 1 ? c.v[e < R - 1 ? e + 1 : 0] : xe));
+            if (N) acc = RN<T>::add(acc, RN<T>::mul(c4, pn.v[e]));
+            out[e] = acc;
+        }
+    }
     // lane-per-row over [r0, r0 + 32) (interface of CsrOp::warp_rows)
     template <class X> __device__ __forceinline__ T warp_rows(int64_t r0, int64_t rend, X x, T *) const {
         const int64_t r = r0 + (threadIdx.x & 31);
