@@ -90,20 +90,40 @@ constexpr int kProfSlots = 16;
 __device__ unsigned long long g_fused_prof[kFMaxCtas * kProfSlots];
 
 // Sense-free grid barrier (all CTAs co-resident by cooperative launch).
+// Release/acquire at GPU scope instead of two full fences: the arrival is an
+// acq_rel atomic (publishes this CTA's partials, which __syncthreads ordered
+// before thread 0's arrival), the last arrival releases the generation word,
+// waiters acquire it.  bar[0] (count) and bar[1] (generation) are the
+// caller's words (bar[0] count, bar[32] generation: the caller's 256-byte
+// counter block).
+__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned *p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned *p, unsigned v) {
+    asm volatile("st.release.gpu.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_gpu(unsigned *p, unsigned v) {
+    asm volatile("st.relaxed.gpu.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ void grid_sync(unsigned *bar, unsigned nb) {
+    unsigned *gen = bar + 32;   // own 128-byte line: polls do not queue behind the arrivals
     __syncthreads();
     if (threadIdx.x == 0) {
-        volatile unsigned *vgen = bar + 1;
-        const unsigned g0 = *vgen;
-        __threadfence();
-        if (atomicAdd(bar, 1u) == nb - 1) {
-            bar[0] = 0u;
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
+        const unsigned g0 = ld_acquire_gpu(gen);
+        if (atom_add_acq_rel_gpu(bar, 1u) == nb - 1) {
+            st_relaxed_gpu(bar, 0u);
+            st_release_gpu(gen, g0 + 1u);
         } else {
-            while (*vgen == g0) __nanosleep(32);
+            while (ld_acquire_gpu(gen) == g0) __nanosleep(20);
         }
-        __threadfence();
     }
     __syncthreads();
 }
