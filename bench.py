@@ -36,10 +36,15 @@ CONFIGS = {
     "C2": ("BentPipe2D", 1500, "BentPipe2D convection-diffusion 1500^2 (2.25M rows)"),
     "C3": ("UniFlow2D", 2500, "UniFlow2D convection-diffusion 2500^2 (6.25M rows)"),
     "C4": ("Laplace3D", 200, "Laplace3D 7-point 200^3 (8M rows)"),
+    "C5": ("synthetic", 4000000, "synthetic irregular nonsymmetric CSR, 4M rows, ~49 nnz/row, + Jacobi(1)"),
 }
+# C5 family calibrated so that fp64 GMRES(50)+J1 needs hundreds of
+# iterations (SURVEY 8(d) warning: the default family converges in 18)
+C5_PARAMS = dict(signs="negative", dominance=1.001, shift=1e-3, far_frac=0.01, band=2000)
 # reference (mpkrylov) iteration counts on these configs (tests/golden/runs.json)
 REF_ITERS = {"C1": {"ir": 200, "fp64": 206}, "C2": {"ir": 10650, "fp64": 10833},
-             "C3": {"ir": None, "fp64": None}, "C4": {"ir": None, "fp64": 4053}}
+             "C3": {"ir": None, "fp64": None}, "C4": {"ir": None, "fp64": 4053},
+             "C5": {"ir": None, "fp64": None}}
 
 
 def peaks():
@@ -94,6 +99,15 @@ class ClockSampler:
         reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(self.rows)}
+
+
+def note(msg):
+    """Progress to stderr (the JSON line stays alone on stdout)."""
+    if os.environ.get("MPK_BENCH_VERBOSE"):
+        print("[bench %.1fs] %s" % (time.perf_counter() - T0, msg), file=sys.stderr, flush=True)
+
+
+T0 = time.perf_counter()
 
 
 def dist_env():
@@ -177,6 +191,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--poly", type=int, default=0, help="GMRES-polynomial preconditioner degree (0: none)")
+    ap.add_argument("--fd", type=int, default=0, help="C5: also time GMRES-FD switching at this iteration")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -202,12 +217,21 @@ def main():
     lib = _lib.load()
     P = mk.Precision
     preset, nx, desc = CONFIGS[args.config]
-    # the reference's beta <= n*u*||w|| test (n*u32 = 0.37 at 6.25M,
-    # 0.48 at 8M rows) declares false breakdowns on C3/C4; they run with "u"
-    rule = "u" if args.config in ("C3", "C4") else "n_u"
-    A = mk.generate_stencil(mk.ProblemSpec(preset, nx))
+    # the reference's beta <= n*u*||w|| test (n*u32 = 0.24 at 4M,
+    # 0.37 at 6.25M, 0.48 at 8M rows) declares false breakdowns on C3-C5;
+    # they run with "u"
+    rule = "u" if args.config in ("C3", "C4", "C5") else "n_u"
+    if args.config == "C5":
+        A = mk.synthetic_irregular(nx, **C5_PARAMS)
+    else:
+        A = mk.generate_stencil(mk.ProblemSpec(preset, nx))
     A_low = mk.convert_matrix(A, P.binary32)
     M32 = M64 = None
+    if args.config == "C5":
+        if world > 1:
+            raise SystemExit("C5 (Jacobi) runs on one GPU")
+        M32 = mk.build_block_jacobi(A_low, 1)   # setup, outside the timed region (cli.py:166-168)
+        M64 = mk.build_block_jacobi(A, 1)
     if args.poly:
         if world > 1:
             raise SystemExit("the polynomial preconditioner runs on one GPU")
@@ -264,8 +288,10 @@ def main():
         barrier()
         return max_over_ranks(ev0.elapsed_time(ev1)), reps
 
+    note("setup done (n=%d)" % n)
     for _ in range(args.warmup):
         rep = solve_ir(b_dev, x0_dev)
+        note("warmup solve: %d iters" % rep.total_iters)
     # timed region: K solves with per-kernel events on the launching stream
     launches0 = lib.mpk_launch_count()
     lib.mpk_prof_reset()
@@ -286,7 +312,8 @@ def main():
     # per Arnoldi step at basis size j: SpMV + CGS2 sv*n*(4j+10); per cycle
     # the correction sv*n*(k+2)
     sv = 4
-    spmv_b = 2.0 * sv * n_loc      # matrix-free stencil: x read + y write
+    # matrix-free stencil: x read + y write; CSR: sv*(nnz+2n) + 4*(nnz+n+1)
+    spmv_b = 2.0 * sv * n_loc if A.stencil is not None else sv * (A.nnz + 2.0 * n) + 4.0 * (A.nnz + n + 1)
     steps_per_cycle = cycle_steps(rep.history)
     alg = sum(sum(spmv_b + sv * n_loc * (4 * (k + 1) + 10) for k in range(st)) + sv * n_loc * (st + 2)
               for st in steps_per_cycle) * args.steps
@@ -347,6 +374,7 @@ def main():
                      "algorithmic_bytes": "per step: stencil SpMV 2*4*n + CGS2 4*n*(4j+10); "
                                           "per cycle: correction 4*n*(k+2) (SURVEY 8(d))"},
     }
+    note("timed IR done")
     if not args.no_fp64:
         solve64 = lambda: solve_64(b_dev, x0_dev)  # noqa: E731
         solve64()
@@ -354,6 +382,7 @@ def main():
         out["fp64_gmres_s"] = ms64 / 1e3
         out["fp64_iters"] = reps64[-1].total_iters
         out["ir_speedup_vs_fp64"] = (ms64 / 1e3) / (ms_step / 1e3)
+    note("fp64 done")
     if not args.no_e2e:
         # public API with host (pinned) inputs; every step copies b and x0 in
         # and the solution out (each rank its own rows when partitioned)
@@ -369,11 +398,25 @@ def main():
         out["e2e"] = {"value": ms_e2e / args.steps / 1e3, "unit": "s", "h2d_bytes_per_step": 2 * 8 * n,
                       "d2h_bytes_per_step": 8 * n, "note": "whole job: b and x0 in, x out (all ranks)"}
     out["clocks"] = clk.summary()
-    if M32 is not None:
+    if args.config == "C5":
+        out["config"]["precond"] = {"kind": "block-jacobi", "block": 1, "fused": "diagonal scaling in k_cycle_reg"}
+        out["config"]["operator"] = "CSR, warp-cooperative bit-exact rows"
+        out["config"]["generator"] = dict(C5_PARAMS, seed=20240817)
+        if args.fd:
+            fcfg = mk.FdConfig(switch_iter=args.fd, low=mk.SolverConfig(m=50, rtol=1e-10, precision=P.binary32,
+                                                                        breakdown_rule=rule,
+                                                                        max_iters=100000),
+                               high=cfg64)
+            solve_fd = lambda: mk.gmres_fd(A, b_dev, x0_dev, fcfg, M_low=M32, M_high=M64, A_low=A_low)  # noqa: E731
+            solve_fd()
+            msfd, repfd = timed(solve_fd, 1)
+            out["fd"] = {"switch_iter": args.fd, "s": msfd / 1e3, "iters": repfd[-1].total_iters,
+                         "converged": bool(repfd[-1].converged)}
+    elif M32 is not None:
         out["config"]["precond"] = {"kind": "gmres-poly", "degree_ir": M32.data.degree,
                                     "degree_fp64": M64.data.degree, "seed": "ones"}
         out["config"]["operator"] = "matrix-free stencil; poly apply = degree SpMVs per step"
-    if rank == 0 and world == 1 and not args.no_cpu and not args.poly:
+    if rank == 0 and world == 1 and not args.no_cpu and not args.poly and args.config != "C5":
         s_it, it, dt = cpu_sample(args.config, "ir", 50)
         full = REF_ITERS[args.config]["ir"] or rep.total_iters
         out["cpu_baseline"] = {"value": s_it * full, "unit": "s", "cores": cpu_cores(), "kind": "port",
