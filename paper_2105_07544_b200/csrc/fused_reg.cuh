@@ -214,8 +214,10 @@ __device__ __noinline__ T phase_a_spmv(const Op &A, const XSlab<T> xs, T *w, int
         // CSR: warp-cooperative 32-row groups (coalesced entries, row-sequential sums)
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         T *sb = sstage + warp * kCsrWarpBuf;
+        // long rows (config 5: ~49 entries): 16 entries per lane in flight (fp32)
+        const bool wide = sizeof(T) == 4 && A.rp[A.n] > 16 * (int64_t)A.n;
         for (int64_t r0 = rb + (int64_t)warp * 32; r0 < re; r0 += (int64_t)kFW * 32) {
-            const T wr = A.warp_rows(r0, re, xs, sb);
+            const T wr = wide ? A.template warp_rows<16>(r0, re, xs, sb) : A.template warp_rows<8>(r0, re, xs, sb);
             if (r0 + lane < re) {
                 w[r0 + lane] = wr;
                 an += wr * wr;

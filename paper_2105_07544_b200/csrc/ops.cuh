@@ -16,10 +16,10 @@
 namespace mpk {
 
 // Products staged per warp for the warp-cooperative CSR rows (elements of T):
-// 8 entries per lane per chunk (16 measured 10% faster on the ~50-entry rows
-// of config 5 in fp32 but 25-35% slower on 5-7-entry stencil rows).
-template <typename T> struct CsrStage { static constexpr int value = 8; };
-constexpr int kCsrWarpBuf = 256;               // staging elements per warp
+// K entries per lane per chunk, 8 by default (16 is ~10% faster on the
+// ~50-entry rows of config 5 in fp32 but 25-35% slower on 5-7-entry stencil
+// rows; callers with long rows pick 16).
+constexpr int kCsrWarpBuf = 512;               // staging elements per warp (K <= 16)
 
 template <typename T> struct CsrOp {
     int64_t n;
@@ -44,8 +44,8 @@ template <typename T> struct CsrOp {
     // csr_matvec (sparse.py:190-206), so bit-identical to row(), at
     // coalesced-load speed for long, irregular rows.  `sb`: kCsrWarpBuf
     // elements of this warp.  Returns the lane's row value (0 past rend).
-    template <class X> __device__ __forceinline__ T warp_rows(int64_t r0, int64_t rend, X x, T *sb) const {
-        constexpr int kCsrStage = CsrStage<T>::value;
+    template <int K = 8, class X> __device__ __forceinline__ T warp_rows(int64_t r0, int64_t rend, X x, T *sb) const {
+        constexpr int kCsrStage = K;
         constexpr int kChunk = 32 * kCsrStage;
         const int lane = threadIdx.x & 31;
         const int64_t last = (r0 + 32 < rend ? r0 + 32 : rend) - 1;
