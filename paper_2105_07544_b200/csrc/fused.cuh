@@ -182,25 +182,42 @@ template <typename T>
 __device__ __forceinline__ void cross_reduce(const T *part, unsigned nb, int ncols, int nslots, T *out,
                                              int stride = kFMaxCtas) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int NQ = (kFSlots + kFW - 1) / kFW;   // slots per warp
+    if (nb <= 160u) {
+        // one CTA per SM (148 on B200): every slot's loads of this warp are
+        // issued before any is reduced (one L2 round trip, not one per slot)
+        constexpr int NI = 5;
+        T v[NQ][NI];
 #pragma unroll
-    for (int q = 0; q < (kFSlots + kFW - 1) / kFW; ++q) {
+        for (int q = 0; q < NQ; ++q) {
+            const int s = warp + kFW * q;
+            const T *p = part + (int64_t)((s < ncols) ? s : kFExtra) * stride;
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {
+                const unsigned b = lane + 32 * i;
+                v[q][i] = (s < nslots && b < nb) ? __ldcg(p + b) : T(0);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            const int s = warp + kFW * q;
+            T acc = T(0);
+#pragma unroll
+            for (int i = 0; i < NI; ++i) acc += v[q][i];
+            acc = warp_sum(acc);
+            if (lane == 0 && s < nslots) out[s] = acc;
+        }
+        return;
+    }
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
         const int s = warp + kFW * q;
         if (s < nslots) {
             const int idx = (s < ncols) ? s : kFExtra;
             const T *p = part + (int64_t)idx * stride;
             T acc = T(0);
-            if (nb <= (unsigned)kFMaxCtas) {
-                T v[kFMaxCtas / 32];
-#pragma unroll
-                for (int i = 0; i < kFMaxCtas / 32; ++i) {
-                    const unsigned b = lane + 32 * i;
-                    v[i] = (b < nb) ? __ldcg(p + b) : T(0);
-                }
-#pragma unroll
-                for (int i = 0; i < kFMaxCtas / 32; ++i) acc += v[i];
-            } else {   // multi-rank: nb = nranks * CTAs per rank columns, same fixed order
-                for (unsigned b = lane; b < nb; b += 32) acc += __ldcg(p + b);
-            }
+            // nb columns (multi-rank: nranks * CTAs per rank), same fixed order
+            for (unsigned b = lane; b < nb; b += 32) acc += __ldcg(p + b);
             acc = warp_sum(acc);
             if (lane == 0) out[s] = acc;
         }

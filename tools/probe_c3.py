@@ -1,4 +1,4 @@
-"""C3 probe: UniFlow2D 2500^2 + GMRES poly(25): setup time, capped IR and
+"""Polynomial-preconditioner probe (default C3: UniFlow2D 2500^2 + GMRES poly(25)): setup time, capped IR and
 fp64 runs (per-iteration time, residual reached)."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -8,13 +8,20 @@ P = mk.Precision
 nx = int(sys.argv[1]) if len(sys.argv) > 1 else 2500
 cap = int(sys.argv[2]) if len(sys.argv) > 2 else 100
 deg = int(sys.argv[3]) if len(sys.argv) > 3 else 25
-A = mk.generate_stencil(mk.ProblemSpec("UniFlow2D", nx))
+preset = sys.argv[4] if len(sys.argv) > 4 else "UniFlow2D"
+A = mk.generate_stencil(mk.ProblemSpec(preset, nx))
 Al = mk.convert_matrix(A, P.binary32)
 t0 = time.time()
-M32 = mk.build_gmres_poly(Al, deg, np.ones(A.n, np.float32), rule="u")
-M64 = mk.build_gmres_poly(A, deg, np.ones(A.n))
+if deg:
+    M32 = mk.build_gmres_poly(Al, deg, np.ones(A.n, np.float32), rule="u")
+    M64 = mk.build_gmres_poly(A, deg, np.ones(A.n))
+else:
+    class _D: degree = 0
+    class _M: data = _D()
+    M32 = M64 = None
 torch.cuda.synchronize()
-print("setup %.2f s, degrees %d / %d" % (time.time() - t0, M32.data.degree, M64.data.degree), flush=True)
+print("%s %d: setup %.2f s, degrees %s / %s" % (preset, nx, time.time() - t0, M32.data.degree if M32 else 0,
+      M64.data.degree if M64 else 0), flush=True)
 b = torch.ones(A.n, dtype=torch.float64, device="cuda"); x0 = torch.zeros_like(b)
 for name, run in (("ir", lambda mi: mk.gmres_ir(A, b, x0, mk.IrConfig(inner=mk.SolverConfig(m=50, rtol=1e-4, precision=P.binary32, max_iters=mi, breakdown_rule="u"), rtol=1e-10), M=M32, A_low=Al)),
                   ("fp64", lambda mi: mk.gmres_restarted(A, M64, b, x0, mk.SolverConfig(m=50, rtol=1e-10, max_iters=mi)))):
