@@ -48,14 +48,20 @@ enum { kRegDots = 0, kRegUpdateDots = 1, kRegUpdateNorm = 2, kRegCorrect = 3 };
 template <typename T, int MODE, int U>
 __device__ __forceinline__ void reg_phase_u(const T *V, int64_t ld, int nc, int64_t rb, int64_t re, int64_t n,
                                             const T *x, T *y, const T *coef, T (&acc)[RegCfg<T>::KP], T &ext,
-                                            const CommArgs<T> *cm, const T *diag) {
+                                            const CommArgs<T> *cm, const T *diag, bool rev) {
     using C = RegCfg<T>;
     constexpr int R = C::R;
     constexpr int KU = C::KP / U;             // columns per part held per row group
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane % C::G, p = lane / C::G;
     constexpr int64_t TRIP = (int64_t)C::WR * U;
-    for (int64_t b = rb + (int64_t)warp * TRIP; b < re; b += (int64_t)kFW * TRIP) {
+    // rev: walk the rows last to first.  Consecutive phases alternate, so each
+    // phase starts on the rows whose basis lines the previous phase touched
+    // last and still finds them in L2 (up to its ~126 MB).
+    const int64_t b0 = rb + (int64_t)warp * TRIP, step = (int64_t)kFW * TRIP;
+    const int64_t ntrip = (b0 < re) ? (re - b0 + step - 1) / step : 0;
+    for (int64_t t = 0; t < ntrip; ++t) {
+        const int64_t b = b0 + (rev ? ntrip - 1 - t : t) * step;
         Pack<T> vv[U][KU];
         Pack<T> xv[U];
 #pragma unroll
@@ -158,13 +164,13 @@ __device__ __forceinline__ void reg_phase_u(const T *V, int64_t ld, int nc, int6
 template <typename T, int MODE>
 __device__ __forceinline__ void reg_phase(const T *V, int64_t ld, int nc, int64_t rb, int64_t re, int64_t n,
                                           const T *x, T *y, const T *coef, T (&acc)[RegCfg<T>::KP], T &ext,
-                                          const CommArgs<T> *cm = nullptr, const T *diag = nullptr) {
+                                          const CommArgs<T> *cm = nullptr, const T *diag = nullptr, bool rev = false) {
     using C = RegCfg<T>;
     const int ncp = (nc + C::P - 1) / C::P;   // columns per part
-    if (ncp * 8 <= C::KP) reg_phase_u<T, MODE, 8>(V, ld, nc, rb, re, n, x, y, coef, acc, ext, cm, diag);
-    else if (ncp * 4 <= C::KP) reg_phase_u<T, MODE, 4>(V, ld, nc, rb, re, n, x, y, coef, acc, ext, cm, diag);
-    else if (ncp * 2 <= C::KP) reg_phase_u<T, MODE, 2>(V, ld, nc, rb, re, n, x, y, coef, acc, ext, cm, diag);
-    else reg_phase_u<T, MODE, 1>(V, ld, nc, rb, re, n, x, y, coef, acc, ext, cm, diag);
+    if (ncp * 8 <= C::KP) reg_phase_u<T, MODE, 8>(V, ld, nc, rb, re, n, x, y, coef, acc, ext, cm, diag, rev);
+    else if (ncp * 4 <= C::KP) reg_phase_u<T, MODE, 4>(V, ld, nc, rb, re, n, x, y, coef, acc, ext, cm, diag, rev);
+    else if (ncp * 2 <= C::KP) reg_phase_u<T, MODE, 2>(V, ld, nc, rb, re, n, x, y, coef, acc, ext, cm, diag, rev);
+    else reg_phase_u<T, MODE, 1>(V, ld, nc, rb, re, n, x, y, coef, acc, ext, cm, diag, rev);
 }
 
 // CTA partials of the register layout: column c lives in part p = c % P,
@@ -414,7 +420,8 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
         __syncthreads();   // w rows of this CTA visible to the other lanes' 16-byte loads
 #pragma unroll
         for (int i = 0; i < C::KP; ++i) acc[i] = T(0);
-        reg_phase<T, kRegDots>(a.V, a.ld, nc, rb, re, a.n, a.w, nullptr, nullptr, acc, ext);
+        reg_phase<T, kRegDots>(a.V, a.ld, nc, rb, re, a.n, a.w, nullptr, nullptr, acc, ext, nullptr, nullptr,
+                               (3 * k) & 1);
         MPK_MARK(2);
         reg_write_partials<T>(acc, nc, an, sred, partA, cmp, 0);
         MPK_SYNC_OR_ABORT();
@@ -425,7 +432,8 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
         // ---------------- phase B: w' = w - V c1 ; c2 = V^T w'
 #pragma unroll
         for (int i = 0; i < C::KP; ++i) acc[i] = T(0);
-        reg_phase<T, kRegUpdateDots>(a.V, a.ld, nc, rb, re, a.n, a.w, a.wp, sc1, acc, ext);
+        reg_phase<T, kRegUpdateDots>(a.V, a.ld, nc, rb, re, a.n, a.w, a.wp, sc1, acc, ext, nullptr, nullptr,
+                                     (3 * k + 1) & 1);
         MPK_MARK(5);
         reg_write_partials<T>(acc, nc, T(0), sred, partB, cmp, pblk);
         MPK_SYNC_OR_ABORT();
@@ -435,7 +443,8 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
         MPK_MARK(7);
         // ---------------- phase C: w'' = w' - V c2 ; ||w''||^2
         T bn = T(0);
-        reg_phase<T, kRegUpdateNorm>(a.V, a.ld, nc, rb, re, a.n, a.wp, a.wpp, sc2, acc, bn, cmp);
+        reg_phase<T, kRegUpdateNorm>(a.V, a.ld, nc, rb, re, a.n, a.wp, a.wpp, sc2, acc, bn, cmp, nullptr,
+                                     (3 * k + 2) & 1);
         MPK_MARK(8);
         reg_write_partials<T>(acc, 0, bn, sred, partC, cmp, 2 * pblk);
         MPK_SYNC_OR_ABORT();
@@ -477,7 +486,8 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
     {
         T acc[C::KP];
         T ext = T(0);
-        reg_phase<T, kRegCorrect>(a.V, a.ld, k, rb, re, a.n, a.x0, a.x_out, sd, acc, ext, nullptr, a.diag);
+        reg_phase<T, kRegCorrect>(a.V, a.ld, k, rb, re, a.n, a.x0, a.x_out, sd, acc, ext, nullptr, a.diag,
+                                  (3 * k) & 1);   // after step k-1's phase C (index 3k-1)
     }
     MPK_MARK(13);
     if (a.prof && tid < kProfSlots) g_fused_prof[blockIdx.x * kProfSlots + tid] = s_prof[tid];
