@@ -273,6 +273,15 @@ int mpk_ir_update(int64_t n, double *x, const float *u, int32_t *changed, void *
 int mpk_precond_apply(const mpk_precond *M, const void *v, void *out, void *stream);
 
 /* ------------------------------------------------------------------ */
+/* host-side setup                                                     */
+/* ------------------------------------------------------------------ */
+/* Reverse Cuthill-McKee permutation of a symmetrized off-diagonal pattern
+ * (row-sorted CSR indptr[n+1] / indices, host memory) into perm[n]; the
+ * permutation of mpkrylov's rcm_ordering (reorder.py:22-63).  Host code, no
+ * device work. */
+int mpk_rcm_host(int64_t n, const int64_t *indptr, const int64_t *indices, int64_t *perm);
+
+/* ------------------------------------------------------------------ */
 /* profiling hooks: per-kernel-class event timing inside mpk_cycle_run */
 /* ------------------------------------------------------------------ */
 /* classes: 0 SpMV+dot1, 1 update1+dot2, 2 update2+norm, 3 normalise, 4 precond,

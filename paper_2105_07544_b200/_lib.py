@@ -28,7 +28,7 @@ EXPORTS = (
     "mpk_cycle_hess_bytes", "mpk_cycle_run", "mpk_residual", "mpk_ir_update",
     "mpk_precond_apply", "mpk_prof_reset", "mpk_prof_read", "mpk_lsq_init", "mpk_lsq_update",
     "mpk_lsq_solve", "mpk_vdiv", "mpk_launch_count", "mpk_fused_prof_read", "mpk_comm_part_bytes",
-    "mpk_dev_alloc", "mpk_dev_free", "mpk_ipc_get", "mpk_ipc_open", "mpk_ipc_close",
+    "mpk_dev_alloc", "mpk_dev_free", "mpk_ipc_get", "mpk_ipc_open", "mpk_ipc_close", "mpk_rcm_host",
 )
 MAX_RANKS = 8
 
@@ -124,6 +124,7 @@ _SIGS["mpk_dev_free"] = (_I32, [_P])
 _SIGS["mpk_ipc_get"] = (_I32, [_P, _P])
 _SIGS["mpk_ipc_open"] = (_I32, [_P, ctypes.POINTER(ctypes.c_void_p)])
 _SIGS["mpk_ipc_close"] = (_I32, [_P])
+_SIGS["mpk_rcm_host"] = (_I32, [_I64, _P, _P, _P])
 _SIGS["mpk_vdiv"] = (_I32, [_I32, _I64, _P, _P, _P, _P])
 _SIGS["mpk_lsq_init"] = (_I32, [_I32, _I32, ctypes.c_double, ctypes.c_double, _P, _P, _P])
 _SIGS["mpk_lsq_update"] = (_I32, [_I32, _I32, _I32, _P, _P, _P, _P, _P, _P])
