@@ -44,13 +44,19 @@ template <typename T> struct alignas(16) Pack {
     T v[16 / sizeof(T)];
 };
 
+// L2-cached 16-byte loads with a 256-byte L2 sector prefetch hint: a warp's
+// 128-byte column segment also pulls in the neighbouring warp's segment
 __device__ __forceinline__ Pack<float> ldcg16(const float *p) {
-    const float4 q = __ldcg(reinterpret_cast<const float4 *>(p));
-    return Pack<float>{{q.x, q.y, q.z, q.w}};
+    Pack<float> r;
+    asm volatile("ld.global.cg.L2::256B.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3])
+                 : "l"(p));
+    return r;
 }
 __device__ __forceinline__ Pack<double> ldcg16(const double *p) {
-    const double2 q = __ldcg(reinterpret_cast<const double2 *>(p));
-    return Pack<double>{{q.x, q.y}};
+    Pack<double> r;
+    asm volatile("ld.global.cg.L2::256B.v2.f64 {%0, %1}, [%2];" : "=d"(r.v[0]), "=d"(r.v[1]) : "l"(p));
+    return r;
 }
 __device__ __forceinline__ void stcg16(float *p, const Pack<float> &v) {
     __stcg(reinterpret_cast<float4 *>(p), make_float4(v.v[0], v.v[1], v.v[2], v.v[3]));
