@@ -216,7 +216,9 @@ __device__ __forceinline__ void cross_reduce(const T *part, unsigned nb, int nco
             const int idx = (s < ncols) ? s : kFExtra;
             const T *p = part + (int64_t)idx * stride;
             T acc = T(0);
-            // nb columns (multi-rank: nranks * CTAs per rank), same fixed order
+            // nb columns (multi-rank: nranks * CTAs per rank), same fixed order;
+            // unrolled so the loads of a slot are in flight together
+#pragma unroll 8
             for (unsigned b = lane; b < nb; b += 32) acc += __ldcg(p + b);
             acc = warp_sum(acc);
             if (lane == 0) out[s] = acc;
