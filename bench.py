@@ -191,7 +191,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--poly", type=int, default=0, help="GMRES-polynomial preconditioner degree (0: none)")
-    ap.add_argument("--fd", type=int, default=0, help="C5: also time GMRES-FD switching at this iteration")
+    ap.add_argument("--fd", type=int, default=0, help="also time GMRES-FD switching precision at this iteration")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -398,20 +398,21 @@ def main():
         out["e2e"] = {"value": ms_e2e / args.steps / 1e3, "unit": "s", "h2d_bytes_per_step": 2 * 8 * n,
                       "d2h_bytes_per_step": 8 * n, "note": "whole job: b and x0 in, x out (all ranks)"}
     out["clocks"] = clk.summary()
+    if args.fd and world == 1:
+        # GMRES-FD (multiprecision.py:236-288): fp32 restarted GMRES for
+        # switch_iter iterations, then fp64 against the original baseline
+        fcfg = mk.FdConfig(switch_iter=args.fd, low=mk.SolverConfig(m=50, rtol=1e-10, precision=P.binary32,
+                                                                    breakdown_rule=rule, max_iters=100000),
+                           high=cfg64)
+        solve_fd = lambda: mk.gmres_fd(A, b_dev, x0_dev, fcfg, M_low=M32, M_high=M64, A_low=A_low)  # noqa: E731
+        solve_fd()
+        msfd, repfd = timed(solve_fd, 1)
+        out["fd"] = {"switch_iter": args.fd, "s": msfd / 1e3, "iters": repfd[-1].total_iters,
+                     "converged": bool(repfd[-1].converged)}
     if args.config == "C5":
         out["config"]["precond"] = {"kind": "block-jacobi", "block": 1, "fused": "diagonal scaling in k_cycle_reg"}
         out["config"]["operator"] = "CSR, warp-cooperative bit-exact rows"
         out["config"]["generator"] = dict(C5_PARAMS, seed=20240817)
-        if args.fd:
-            fcfg = mk.FdConfig(switch_iter=args.fd, low=mk.SolverConfig(m=50, rtol=1e-10, precision=P.binary32,
-                                                                        breakdown_rule=rule,
-                                                                        max_iters=100000),
-                               high=cfg64)
-            solve_fd = lambda: mk.gmres_fd(A, b_dev, x0_dev, fcfg, M_low=M32, M_high=M64, A_low=A_low)  # noqa: E731
-            solve_fd()
-            msfd, repfd = timed(solve_fd, 1)
-            out["fd"] = {"switch_iter": args.fd, "s": msfd / 1e3, "iters": repfd[-1].total_iters,
-                         "converged": bool(repfd[-1].converged)}
     elif M32 is not None:
         out["config"]["precond"] = {"kind": "gmres-poly", "degree_ir": M32.data.degree,
                                     "degree_fp64": M64.data.degree, "seed": "ones"}

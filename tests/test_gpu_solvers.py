@@ -220,3 +220,17 @@ def test_c1_laplace3d40_counts(cuda, runs):
     inner = mk.SolverConfig(m=50, rtol=1e-4, precision=P.binary32, max_iters=20000, breakdown_rule="u")
     rep = mk.gmres_ir(A, b, np.zeros(A.n), mk.IrConfig(inner=inner, rtol=1e-10))
     compare(rep, runs["ir_l3d40_rule_u"], hist="fp32", exact_iters=False, slack=50)
+
+
+def test_run_to_run_bit_identical(cuda):
+    """SPEC determinism: fixed-order reductions everywhere, so two solves of
+    the same system give bit-identical histories and solutions."""
+    A = L("BentPipe2D", 96)
+    b = np.ones(A.n)
+    r1, r2 = ir(A, b), ir(A, b)
+    assert [(h.implicit_relres, h.explicit_relres) for h in r1.history] == \
+        [(h.implicit_relres, h.explicit_relres) for h in r2.history]
+    assert r1.x.tobytes() == r2.x.tobytes()
+    g1 = gm(A, b, m=50, rtol=1e-10)
+    g2 = gm(A, b, m=50, rtol=1e-10)
+    assert g1.x.tobytes() == g2.x.tobytes() and g1.total_iters == g2.total_iters
