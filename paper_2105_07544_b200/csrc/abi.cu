@@ -91,7 +91,12 @@ struct Ws {
     float *partials_low;
     void *sums;
 };
-int64_t ws_partials_bytes() { return (int64_t)max_blocks() * kStride * 8; }
+// also holds the persistent cycle's 3 phases x (m + 2) slots x 320 CTAs (m <= 511)
+int64_t ws_partials_bytes() {
+    const int64_t multi = (int64_t)max_blocks() * kStride * 8;
+    const int64_t cycle = 3LL * (MPK_MAX_STEPS + 2) * kFMaxCtas * 8;
+    return multi > cycle ? multi : cycle;
+}
 int64_t ws_low_bytes() { return (int64_t)max_blocks() * 2 * 4; }
 Ws carve(void *base) {
     char *p = (char *)base;
@@ -620,17 +625,20 @@ int launch_fused_reg(const Op &op, const mpk_cycle_desc *d, int cap, double tf, 
     const int m = d->m;
     T *w = (T *)d->work;
     Ws ws = carve(d->ws);
-    auto kern = k_cycle_reg<T, Op>;
-    const size_t smem =
-        sizeof(T) * ((size_t)(m + 1) * m + 2 * m + (m + 1) + 2 * kFSlots + kFW * kFSlots + kFW * kCsrWarpBuf);
-    static size_t attr_set = 0;
-    if (smem > attr_set) {
+    // layout of k_cycle_reg: small m keeps R (m+1 x m) in shared memory
+    const bool big = m + 1 > kRegMaxCols;
+    auto kern = big ? k_cycle_reg<T, Op, true> : k_cycle_reg<T, Op, false>;
+    const size_t nslot = big ? (size_t)m + 2 : (size_t)kFSlots;
+    const size_t smem = sizeof(T) * ((big ? 0 : (size_t)(m + 1) * m) + 2 * m + (m + 1) + 2 * nslot + kFW * kFSlots +
+                                     (big ? nslot : 0) + kFW * kCsrWarpBuf);
+    static size_t attr_set[2] = {0, 0};
+    if (smem > attr_set[big]) {
         cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (ea != cudaSuccess) {
             g_err = std::string("k_cycle_reg smem attribute: ") + cudaGetErrorString(ea);
             return MPK_ELAUNCH;
         }
-        attr_set = smem;
+        attr_set[big] = smem;
     }
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFB, smem);
@@ -730,6 +738,14 @@ template <typename T> int run_cycle(const mpk_cycle_desc *d, cudaStream_t s) {
     // register kernel applies it inside its SpMV input and correction
     const bool diag1 = precond && d->M->kind == MPK_PC_JACOBI && d->M->block == 1 && d->M->n == n &&
                        d->M->dtype == d->dtype;
+    // identity preconditioner, any m: the persistent register kernel (column
+    // blocks beyond 51 columns); MPK_FUSED_IMPL=tma keeps the TMA ring for m <= 63
+    if (!precond && !(d->flags & 4) && !fused_use_tma() && (uintptr_t)d->x_out % 16 == 0 &&
+        (uintptr_t)d->V % 16 == 0 && (uintptr_t)d->work % 16 == 0 && (uintptr_t)d->r0 % 16 == 0) {
+        return with_op<T>(d->A, [&](auto op) -> int {
+            return launch_fused_reg<T, decltype(op)>(op, d, cap, tf, u, s);
+        });
+    }
     if (diag1 && m + 1 <= kRegMaxCols && !(d->flags & 4) && !fused_use_tma() &&
         (uintptr_t)d->x_out % 16 == 0 && (uintptr_t)d->V % 16 == 0 && (uintptr_t)d->work % 16 == 0 &&
         (uintptr_t)d->r0 % 16 == 0 && (uintptr_t)d->M->lu % 16 == 0) {

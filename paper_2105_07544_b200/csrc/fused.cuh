@@ -180,18 +180,20 @@ __device__ __forceinline__ bool grid_sync_x(unsigned *bar, unsigned nb, const Co
 // lanes stride the CTAs, then a fixed butterfly: identical in every CTA.
 template <typename T>
 __device__ __forceinline__ void cross_reduce(const T *part, unsigned nb, int ncols, int nslots, T *out,
-                                             int stride = kFMaxCtas) {
+                                             int stride = kFMaxCtas, int xslot = kFExtra) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int NQ = (kFSlots + kFW - 1) / kFW;   // slots per warp
     if (nb <= 160u) {
-        // one CTA per SM (148 on B200): every slot's loads of this warp are
-        // issued before any is reduced (one L2 round trip, not one per slot)
+      // one CTA per SM (148 on B200): every slot's loads of this warp are
+      // issued before any is reduced (one L2 round trip, not one per slot);
+      // more than NQ * kFW slots (m > 78) go in rounds
+      for (int s0 = 0; s0 < nslots; s0 += NQ * kFW) {
         constexpr int NI = 5;
         T v[NQ][NI];
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
-            const int s = warp + kFW * q;
-            const T *p = part + (int64_t)((s < ncols) ? s : kFExtra) * stride;
+            const int s = s0 + warp + kFW * q;
+            const T *p = part + (int64_t)((s < ncols) ? s : xslot) * stride;
 #pragma unroll
             for (int i = 0; i < NI; ++i) {
                 const unsigned b = lane + 32 * i;
@@ -200,20 +202,21 @@ __device__ __forceinline__ void cross_reduce(const T *part, unsigned nb, int nco
         }
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
-            const int s = warp + kFW * q;
+            const int s = s0 + warp + kFW * q;
             T acc = T(0);
 #pragma unroll
             for (int i = 0; i < NI; ++i) acc += v[q][i];
             acc = warp_sum(acc);
             if (lane == 0 && s < nslots) out[s] = acc;
         }
-        return;
+      }
+      return;
     }
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
         const int s = warp + kFW * q;
         if (s < nslots) {
-            const int idx = (s < ncols) ? s : kFExtra;
+            const int idx = (s < ncols) ? s : xslot;
             const T *p = part + (int64_t)idx * stride;
             T acc = T(0);
             // nb columns (multi-rank: nranks * CTAs per rank), same fixed order;

@@ -81,6 +81,9 @@ __device__ __forceinline__ void reg_phase_u(const T *V, int64_t ld, int nc, int6
 #pragma unroll
                 for (int e = 0; e < R; ++e)
                     xv[u].v[e] = (p == 0 && live && r + e < n) ? x[r + e] : T(0);   // x may alias y
+            } else if (MODE == kRegUpdateNorm && p != 0) {
+#pragma unroll
+                for (int e = 0; e < R; ++e) xv[u].v[e] = T(0);   // only part 0 uses x (x may alias y)
             } else if (live) {
                 xv[u] = ldcg16(x + r);
             } else {
@@ -178,12 +181,16 @@ __device__ __forceinline__ void reg_phase(const T *V, int64_t ld, int nc, int64_
 // `part` is this CTA's column of the local buffer (single GPU); with a comm,
 // the CTA's column rank * nb + cta of the phase's block in EVERY rank's
 // buffer is written (P2P stores; `off` = the phase block's element offset).
+// Column block form (m > 51): the block's columns land at c0 + c and the
+// extra scalar, if has_extra, at slot xslot.
 template <typename T>
 __device__ __forceinline__ void reg_write_partials(T (&acc)[RegCfg<T>::KP], int nc, T extra, T *sm, T *part,
-                                                   const CommArgs<T> *cm = nullptr, int64_t off = 0) {
+                                                   const CommArgs<T> *cm = nullptr, int64_t off = 0, int c0 = 0,
+                                                   bool has_extra = true, int xslot = kFExtra) {
     using C = RegCfg<T>;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane % C::G, p = lane / C::G;
+    if (c0 != 0 || !has_extra) __syncthreads();   // block form: sm reused by consecutive calls
 #pragma unroll
     for (int i = 0; i < C::KP; ++i) {
         T v = acc[i];
@@ -196,11 +203,12 @@ __device__ __forceinline__ void reg_write_partials(T (&acc)[RegCfg<T>::KP], int 
     if (lane == 0) sm[warp * kFSlots + kFExtra] = e;
     __syncthreads();
     for (int c = threadIdx.x; c < kFSlots; c += kFB) {
-        if (c < nc || c == kFExtra) {
+        if (c < nc || (c == kFExtra && has_extra)) {
             T s = sm[c];
             for (int w = 1; w < kFW; ++w) s += sm[w * kFSlots + c];
             if (cm == nullptr) {
-                part[(int64_t)c * kFMaxCtas + blockIdx.x] = s;
+                const int slot = (c == kFExtra) ? xslot : c0 + c;
+                part[(int64_t)slot * kFMaxCtas + blockIdx.x] = s;
             } else {
                 const int64_t col = (int64_t)cm->rank * gridDim.x + blockIdx.x;
                 for (int q = 0; q < cm->nranks; ++q) cm->part[q][off + (int64_t)c * kXStride + col] = s;
@@ -265,19 +273,27 @@ __device__ __noinline__ T phase_a_spmv(const Op &A, const XSlab<T> xs, T *w, int
     return an;
 }
 
-template <typename T, class Op>
+template <typename T, class Op, bool BIG>
 __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
     using C = RegCfg<T>;
     extern __shared__ __align__(16) unsigned char dsm_reg[];
     const int m = a.m, ldr = m + 1;
-    T *sR = reinterpret_cast<T *>(dsm_reg);    // (m+1) x m rotated columns
-    T *scs = sR + (int64_t)ldr * m;
+    // big (m + 1 > 52 columns): the basis is streamed in blocks of 52 columns
+    // (phase B as an update pass plus a dot pass), the rotated Hessenberg R
+    // lives in global memory (a.H.h, identical copies written by every CTA),
+    // the per-step vectors stay in shared memory
+    constexpr bool big = BIG;   // instantiated separately: m + 1 > 52
+    const int nslot = big ? m + 2 : kFSlots;   // c1 / c2 vector length
+    T *sR = big ? a.H.h : reinterpret_cast<T *>(dsm_reg);    // (m+1) x m rotated columns
+    T *scs = big ? reinterpret_cast<T *>(dsm_reg) : sR + (int64_t)ldr * m;
     T *ssn = scs + m;
     T *sg = ssn + m;                           // m + 1
-    T *sc1 = sg + (m + 1);                     // kFSlots
-    T *sc2 = sc1 + kFSlots;                    // kFSlots
-    T *sred = sc2 + kFSlots;                   // kFW * kFSlots
-    T *sstage = sred + kFW * kFSlots;          // kFW * kCsrWarpBuf (CSR SpMV staging)
+    T *sc1 = sg + (m + 1);                     // nslot
+    T *sc2 = sc1 + nslot;                      // nslot
+    T *sred = sc2 + nslot;                     // kFW * kFSlots
+    T *sctmp = sred + kFW * kFSlots;           // big: nslot (the column being rotated)
+    T *sstage = sctmp + (big ? nslot : 0);     // kFW * kCsrWarpBuf (CSR SpMV staging)
+    const int xslot = big ? m + 1 : kFExtra;   // partial slot of the extra scalar
     __shared__ T s_gamma, s_beta, s_bn2;
     __shared__ int s_done, s_steps, s_break, s_app;
     __shared__ double s_scale;
@@ -304,7 +320,7 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
     const CommArgs<T> *cmp = multi ? &a.cm : nullptr;
     // partials: single GPU -> local [slot][cta]; multi -> every rank's
     // [phase][slot][rank * nb + cta], reduced over nranks * nb columns
-    const int64_t pblk = multi ? (int64_t)kFSlots * kXStride : (int64_t)kFSlots * kFMaxCtas;
+    const int64_t pblk = multi ? (int64_t)kFSlots * kXStride : (int64_t)nslot * kFMaxCtas;
     T *pbase = multi ? a.cm.part[a.cm.rank] : a.part;
     T *partA = pbase, *partB = pbase + pblk, *partC = pbase + 2 * pblk;
     const unsigned ncol = multi ? nb * (unsigned)a.cm.nranks : nb;
@@ -418,48 +434,102 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
         an = phase_a_spmv<T>(A, XSlab<T>{src, vk, dv, rb, re, a.diag, a.z}, a.w, rb, re, sstage);
         MPK_MARK(1);
         __syncthreads();   // w rows of this CTA visible to the other lanes' 16-byte loads
+        const int nbk = BIG ? (nc + kRegMaxCols - 1) / kRegMaxCols : 1;   // column blocks
+        auto blk = [&](int bi, int total, int &c0, int &cn) {
+            c0 = bi * kRegMaxCols;
+            cn = (total - c0 < kRegMaxCols) ? total - c0 : kRegMaxCols;
+        };
+        if (!BIG) {
 #pragma unroll
-        for (int i = 0; i < C::KP; ++i) acc[i] = T(0);
-        reg_phase<T, kRegDots>(a.V, a.ld, nc, rb, re, a.n, a.w, nullptr, nullptr, acc, ext, nullptr, nullptr,
-                               (3 * k) & 1);
-        MPK_MARK(2);
-        reg_write_partials<T>(acc, nc, an, sred, partA, cmp, 0);
+            for (int i = 0; i < C::KP; ++i) acc[i] = T(0);
+            reg_phase<T, kRegDots>(a.V, a.ld, nc, rb, re, a.n, a.w, nullptr, nullptr, acc, ext, nullptr, nullptr,
+                                   (3 * k) & 1);
+            MPK_MARK(2);
+            reg_write_partials<T>(acc, nc, an, sred, partA, cmp, 0, 0, true, xslot);
+        } else {
+            for (int bi = 0; bi < nbk; ++bi) {
+                int c0, cn;
+                blk(bi, nc, c0, cn);
+#pragma unroll
+                for (int i = 0; i < C::KP; ++i) acc[i] = T(0);
+                reg_phase<T, kRegDots>(a.V + (int64_t)c0 * a.ld, a.ld, cn, rb, re, a.n, a.w, nullptr, nullptr, acc,
+                                       ext);
+                reg_write_partials<T>(acc, cn, an, sred, partA, nullptr, 0, c0, bi == nbk - 1, xslot);
+            }
+            MPK_MARK(2);
+        }
         MPK_SYNC_OR_ABORT();
         MPK_MARK(3);
-        cross_reduce<T>(partA, ncol, nc, nc + 1, sc1, pstride);   // sc1[0..k], sc1[nc] = ||w||^2
+        cross_reduce<T>(partA, ncol, nc, nc + 1, sc1, pstride, xslot);   // sc1[0..k], sc1[nc] = ||w||^2
         __syncthreads();
         MPK_MARK(4);
         // ---------------- phase B: w' = w - V c1 ; c2 = V^T w'
+        if (!BIG) {
 #pragma unroll
-        for (int i = 0; i < C::KP; ++i) acc[i] = T(0);
-        reg_phase<T, kRegUpdateDots>(a.V, a.ld, nc, rb, re, a.n, a.w, a.wp, sc1, acc, ext, nullptr, nullptr,
-                                     (3 * k + 1) & 1);
-        MPK_MARK(5);
-        reg_write_partials<T>(acc, nc, T(0), sred, partB, cmp, pblk);
+            for (int i = 0; i < C::KP; ++i) acc[i] = T(0);
+            reg_phase<T, kRegUpdateDots>(a.V, a.ld, nc, rb, re, a.n, a.w, a.wp, sc1, acc, ext, nullptr, nullptr,
+                                         (3 * k + 1) & 1);
+            MPK_MARK(5);
+            reg_write_partials<T>(acc, nc, T(0), sred, partB, cmp, pblk, 0, true, xslot);
+        } else {
+            // w' accumulated block by block in place (an update pass), then the
+            // dot pass V^T w' (the basis is read twice in this phase)
+            for (int bi = 0; bi < nbk; ++bi) {
+                int c0, cn;
+                blk(bi, nc, c0, cn);
+                T dummy = T(0);
+                reg_phase<T, kRegUpdateNorm>(a.V + (int64_t)c0 * a.ld, a.ld, cn, rb, re, a.n, bi ? a.wp : a.w, a.wp,
+                                             sc1 + c0, acc, dummy);
+                __syncthreads();
+            }
+            for (int bi = 0; bi < nbk; ++bi) {
+                int c0, cn;
+                blk(bi, nc, c0, cn);
+#pragma unroll
+                for (int i = 0; i < C::KP; ++i) acc[i] = T(0);
+                reg_phase<T, kRegDots>(a.V + (int64_t)c0 * a.ld, a.ld, cn, rb, re, a.n, a.wp, nullptr, nullptr, acc,
+                                       ext);
+                reg_write_partials<T>(acc, cn, T(0), sred, partB, nullptr, pblk, c0, false, xslot);
+            }
+            MPK_MARK(5);
+        }
         MPK_SYNC_OR_ABORT();
         MPK_MARK(6);
-        cross_reduce<T>(partB, ncol, nc, nc, sc2, pstride);
+        cross_reduce<T>(partB, ncol, nc, nc, sc2, pstride, xslot);
         __syncthreads();
         MPK_MARK(7);
         // ---------------- phase C: w'' = w' - V c2 ; ||w''||^2
         T bn = T(0);
-        reg_phase<T, kRegUpdateNorm>(a.V, a.ld, nc, rb, re, a.n, a.wp, a.wpp, sc2, acc, bn, cmp, nullptr,
-                                     (3 * k + 2) & 1);
+        if (!BIG) {
+            reg_phase<T, kRegUpdateNorm>(a.V, a.ld, nc, rb, re, a.n, a.wp, a.wpp, sc2, acc, bn, cmp, nullptr,
+                                         (3 * k + 2) & 1);
+        } else {
+            for (int bi = 0; bi < nbk; ++bi) {
+                int c0, cn;
+                blk(bi, nc, c0, cn);
+                T dummy = T(0);
+                reg_phase<T, kRegUpdateNorm>(a.V + (int64_t)c0 * a.ld, a.ld, cn, rb, re, a.n, bi ? a.wpp : a.wp,
+                                             a.wpp, sc2 + c0, acc, bi == nbk - 1 ? bn : dummy);
+                __syncthreads();
+            }
+        }
         MPK_MARK(8);
-        reg_write_partials<T>(acc, 0, bn, sred, partC, cmp, 2 * pblk);
+        reg_write_partials<T>(acc, 0, bn, sred, partC, cmp, 2 * pblk, 0, true, xslot);
         MPK_SYNC_OR_ABORT();
         MPK_MARK(9);
-        cross_reduce<T>(partC, ncol, 0, 1, &s_bn2, pstride);
+        cross_reduce<T>(partC, ncol, 0, 1, &s_bn2, pstride, xslot);
         __syncthreads();
         MPK_MARK(10);
         // ---------------- beta, append test, Givens (every CTA, identical)
-        T *col = sR + (int64_t)k * ldr;
+        T *col = big ? sctmp : sR + (int64_t)k * ldr;
         for (int i = tid; i < nc; i += kFB) col[i] = RN<T>::add(sc1[i], sc2[i]);
         __syncthreads();
         if (tid == 0)
             givens_step<T>(a, k, nc, ldr, col, s_bn2, sc1[nc], s_scale, lead, scs, ssn, sg, s_beta, s_steps, s_done,
                            s_break);
         __syncthreads();
+        if (big)   // every CTA keeps its own (identical) copy of R in global memory
+            for (int i = tid; i <= nc; i += kFB) sR[(int64_t)k * ldr + i] = col[i];
     }
 
     MPK_MARK(11);
@@ -472,7 +542,8 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
     if (k > 0 && s_app) return;   // TriangularBreakdownError: x_out untouched
     if (lead) {
         for (int i = tid; i < k; i += kFB) a.H.d[i] = sd[i];
-        for (int i = tid; i < k * ldr; i += kFB) a.H.h[i] = sR[i];
+        if (!big)
+            for (int i = tid; i < k * ldr; i += kFB) a.H.h[i] = sR[i];
         for (int i = tid; i <= k; i += kFB) a.H.g[i] = sg[i];
     }
     if (a.final_col && k > 0 && !s_break) {
@@ -486,8 +557,17 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
     {
         T acc[C::KP];
         T ext = T(0);
-        reg_phase<T, kRegCorrect>(a.V, a.ld, k, rb, re, a.n, a.x0, a.x_out, sd, acc, ext, nullptr, a.diag,
-                                  (3 * k) & 1);   // after step k-1's phase C (index 3k-1)
+        if (!BIG) {
+            reg_phase<T, kRegCorrect>(a.V, a.ld, k, rb, re, a.n, a.x0, a.x_out, sd, acc, ext, nullptr, a.diag,
+                                      (3 * k) & 1);   // after step k-1's phase C (index 3k-1)
+        } else {   // big: x += V_b d_b block by block (no diagonal preconditioner here)
+            for (int c0 = 0; c0 < k; c0 += kRegMaxCols) {
+                const int cn = (k - c0 < kRegMaxCols) ? k - c0 : kRegMaxCols;
+                reg_phase<T, kRegCorrect>(a.V + (int64_t)c0 * a.ld, a.ld, cn, rb, re, a.n, c0 ? a.x_out : a.x0,
+                                          a.x_out, sd + c0, acc, ext);
+                __syncthreads();
+            }
+        }
     }
     MPK_MARK(13);
     if (a.prof && tid < kProfSlots) g_fused_prof[blockIdx.x * kProfSlots + tid] = s_prof[tid];

@@ -9,6 +9,7 @@ ap.add_argument("--config", default="C2")
 ap.add_argument("--solver", default="ir")
 ap.add_argument("--max-iters", type=int, default=1000)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--m", type=int, default=50)
 a = ap.parse_args()
 spec = {"C1": ("Laplace3D", 40), "C2": ("BentPipe2D", 1500), "C4": ("Laplace3D", 200),
         "C3": ("UniFlow2D", 2500)}[a.config]
@@ -17,10 +18,10 @@ b = torch.ones(A.n, dtype=torch.float64, device="cuda"); x0 = torch.zeros_like(b
 P = mk.Precision
 if a.solver == "ir":
     Al = mk.convert_matrix(A, P.binary32)
-    inner = mk.SolverConfig(m=50, rtol=1e-4, precision=P.binary32, max_iters=a.max_iters)
+    inner = mk.SolverConfig(m=a.m, rtol=1e-4, precision=P.binary32, max_iters=a.max_iters)
     run = lambda: mk.gmres_ir(A, b, x0, mk.IrConfig(inner=inner, rtol=1e-10), A_low=Al)
 else:
-    run = lambda: mk.gmres_restarted(A, None, b, x0, mk.SolverConfig(m=50, rtol=1e-10, max_iters=a.max_iters))
+    run = lambda: mk.gmres_restarted(A, None, b, x0, mk.SolverConfig(m=a.m, rtol=1e-10, max_iters=a.max_iters))
 run()
 best = 1e30
 for _ in range(a.reps):
@@ -28,5 +29,5 @@ for _ in range(a.reps):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(); rep = run(); e1.record(); torch.cuda.synchronize()
     best = min(best, e0.elapsed_time(e1))
-print("%s %s TR=%s iters %d relres %.3e  %.2f ms  %.1f us/iter" % (a.config, a.solver, os.environ.get("MPK_FUSED_TR", "default"),
+print("%s %s m=%d TR=%s iters %d relres %.3e  %.2f ms  %.1f us/iter" % (a.config, a.solver, a.m, os.environ.get("MPK_FUSED_TR", "default"),
       rep.total_iters, rep.final_explicit_relres, best, best * 1e3 / rep.total_iters))
