@@ -1,5 +1,6 @@
 // Persistent cooperative cycle kernel, register-streaming variant
-// (gmres.py:134-205 with kernels.py:98-216; identity preconditioner, m <= 51).
+// (gmres.py:134-205 with kernels.py:98-216; identity or diagonal preconditioner;
+// any m: beyond 51 the basis is streamed in 52-column blocks, BIG instantiation).
 //
 // Same phase structure, grid barriers, fixed-order cross-CTA reductions and
 // redundant per-CTA Givens as k_cycle_fused (fused.cuh), but the basis is
@@ -24,7 +25,7 @@
 
 namespace mpk {
 
-constexpr int kRegMaxCols = 52;          // m + 1 <= 52 (m <= 51); wider bases use k_cycle_fused
+constexpr int kRegMaxCols = 52;          // columns per streaming block (one pass per phase when m <= 51)
 
 template <typename T> struct RegCfg {
     static constexpr int R = 16 / (int)sizeof(T);      // rows per 16-byte group (4 fp32 / 2 fp64)
