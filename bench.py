@@ -397,6 +397,33 @@ def main():
         assert not xs_e[-1].is_cuda
         out["e2e"] = {"value": ms_e2e / args.steps / 1e3, "unit": "s", "h2d_bytes_per_step": 2 * 8 * n,
                       "d2h_bytes_per_step": 8 * n, "note": "whole job: b and x0 in, x out (all ranks)"}
+    if world == 1 and A.stencil is not None:
+        # SpMV GB/s (the metric's second half): standalone mpk_spmv on this
+        # matrix, stencil and CSR forms, fp64 and fp32, algorithmic bytes of
+        # SURVEY 8(d) (CSR) / x read + y write (stencil), CUDA events
+        from paper_2105_07544_b200.sparse import spmv_into
+
+        spmv_rates = {}
+        for prec, M in ((P.binary64, A), (P.binary32, A_low)):
+            xs = torch.randn(n, dtype=prec.torch_dtype, device="cuda")
+            ys = torch.empty_like(xs)
+            svb = 8 if prec is P.binary64 else 4
+            for form in ("stencil", "csr"):
+                M.use_stencil = form == "stencil"
+                spmv_into(M, xs, ys)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(20):
+                    spmv_into(M, xs, ys)
+                e1.record()
+                torch.cuda.synchronize()
+                ms = e0.elapsed_time(e1) / 20
+                byt = 2.0 * svb * n if form == "stencil" else svb * (M.nnz + 2.0 * n) + 4.0 * (M.nnz + n + 1)
+                spmv_rates["%s_%s" % (form, prec.value)] = {"ms": ms, "GBs": byt / ms / 1e6,
+                                                            "frac": byt / ms / 1e6 / peak}
+            M.use_stencil = True
+        out["spmv"] = spmv_rates
     out["clocks"] = clk.summary()
     if args.fd and world == 1:
         # GMRES-FD (multiprecision.py:236-288): fp32 restarted GMRES for

@@ -58,7 +58,22 @@ __device__ __forceinline__ int64_t gstride() { return (int64_t)gridDim.x * block
 template <typename T, class Op, class X, class F>
 __device__ __forceinline__ void for_rows(const Op &A, X x, T *sb, F &&fn) {
     if constexpr (Op::kStencil) {
-        for (int64_t r = gtid(); r < A.n; r += gstride()) fn(r, A.row(r, x));
+        constexpr int R = 16 / (int)sizeof(T);
+        if (A.group_ok() && ((uintptr_t)x.p % 16) == 0) {
+            // 16-byte row groups (vector reads of the group and its N/S/B/U
+            // neighbours), bit-identical to row(); scalar tail past n - n % R
+            const int64_t ng = A.n / R;
+            auto xv = [&](int64_t c) { return x.vec(c); };
+            for (int64_t gi = gtid(); gi < ng; gi += gstride()) {
+                T o[R];
+                A.row_group(gi * R, xv, x, o);
+#pragma unroll
+                for (int e = 0; e < R; ++e) fn(gi * R + e, o[e]);
+            }
+            for (int64_t r = ng * R + gtid(); r < A.n; r += gstride()) fn(r, A.row(r, x));
+        } else {
+            for (int64_t r = gtid(); r < A.n; r += gstride()) fn(r, A.row(r, x));
+        }
     } else {
         const int lane = threadIdx.x & 31;
         const int64_t gw = gtid() >> 5, nw = gstride() >> 5;

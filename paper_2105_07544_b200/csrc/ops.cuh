@@ -271,12 +271,19 @@ template <typename T> struct StencilOp {
 template <typename T> struct XPlain {
     const T *__restrict__ p;
     __device__ __forceinline__ T operator()(int64_t c) const { return p[c]; }
+    __device__ __forceinline__ Pack<T> vec(int64_t c) const { return *reinterpret_cast<const Pack<T> *>(p + c); }
 };
 // x = src / d, exactly the reference's basis column w / beta (kernels.py:125)
 template <typename T> struct XScaled {
     const T *__restrict__ p;
     T d;
     __device__ __forceinline__ T operator()(int64_t c) const { return RN<T>::div(p[c], d); }
+    __device__ __forceinline__ Pack<T> vec(int64_t c) const {
+        Pack<T> q = *reinterpret_cast<const Pack<T> *>(p + c);
+#pragma unroll
+        for (int e = 0; e < (int)(16 / sizeof(T)); ++e) q.v[e] = RN<T>::div(q.v[e], d);
+        return q;
+    }
 };
 // same, reading through L2 (data written by other CTAs of a persistent kernel)
 template <typename T> struct XScaledCG {
