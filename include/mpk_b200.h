@@ -230,7 +230,8 @@ typedef struct mpk_cycle_desc {
     int32_t nranks;         /* 1, or > 1 with `comm` (row-partitioned; identity preconditioner) */
     int32_t flags;          /* bit0: per-kernel event timing; bit1: write the last basis column;
                                bit2: force the multi-kernel cycle (no persistent kernel);
-                               bit3: phase profiler of the persistent kernel */
+                               bit3: phase profiler of the persistent kernel;
+                               bit4: lagged one-reduction CGS2 (identity preconditioner, m <= 51) */
     const mpk_comm *comm;   /* nranks > 1: this rank's view of the communicator */
 } mpk_cycle_desc;
 

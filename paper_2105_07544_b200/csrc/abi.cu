@@ -17,7 +17,7 @@
 #include <utility>
 #include <vector>
 
-#include "fused_reg.cuh"
+#include "fused_dcgs2.cuh"
 
 using namespace mpk;
 
@@ -707,6 +707,65 @@ int launch_fused_reg(const Op &op, const mpk_cycle_desc *d, int cap, double tf, 
     return check_launch("k_cycle_reg");
 }
 
+// Lagged one-reduction CGS2 (desc flag bit 4, SolverConfig.orthogonalization
+// = "dcgs2"): identity preconditioner, m <= 51, one GPU.
+template <typename T, class Op>
+int launch_dcgs2(const Op &op, const mpk_cycle_desc *d, int cap, double tf, double u, cudaStream_t s) {
+    const int m = d->m;
+    T *w = (T *)d->work;
+    Ws ws = carve(d->ws);
+    auto kern = k_cycle_dcgs2<T, Op>;
+    const size_t smem = sizeof(T) * (2 * (size_t)(m + 1) * m + 2 * m + (m + 1) + 5 * 64 + kFW * kFSlots +
+                                     kFW * kCsrWarpBuf);
+    static size_t attr_set = 0;
+    if (smem > attr_set) {
+        cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (ea != cudaSuccess) {
+            g_err = std::string("k_cycle_dcgs2 smem attribute: ") + cudaGetErrorString(ea);
+            return MPK_ELAUNCH;
+        }
+        attr_set = smem;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFB, smem);
+    if (per_sm < 1) return fail(MPK_ELAUNCH, "dcgs2 cycle kernel does not fit on an SM");
+    int grid = sm_count_cached();
+    if (grid > 160) grid = 160;   // cross_reduce fast path
+    grid = fused_grid(grid, d->n);
+    FusedArgs<T> fa;
+    memset(&fa, 0, sizeof(fa));
+    fa.n = d->n;
+    fa.ld = d->ld;
+    fa.m = m;
+    fa.cap = cap;
+    fa.V = (T *)d->V;
+    fa.r0 = (const T *)d->r0;
+    fa.rnorm2 = (const T *)d->rnorm2;
+    fa.x0 = (const T *)d->x0;
+    fa.x_out = (T *)d->x_out;
+    fa.w = w;
+    fa.wp = w + d->ld;
+    fa.wpp = w + 2 * d->ld;
+    fa.part = (T *)ws.partials;
+    fa.bar = ws.counters + 8;
+    fa.H = hess_view<T>(d->hess, m);
+    fa.ctl = d->ctl;
+    fa.tf = tf;
+    fa.exit_tol = d->exit_tol;
+    fa.norm_scale = d->norm_scale;
+    fa.u = u;
+    fa.cm.nranks = 1;
+    Op opc = op;
+    void *args[] = {(void *)&opc, (void *)&fa};
+    ProfScope ps(7, 0.0, s);
+    cudaError_t e = cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(kFB), args, smem, s);
+    if (e != cudaSuccess) {
+        g_err = std::string("k_cycle_dcgs2: ") + cudaGetErrorString(e);
+        return MPK_ELAUNCH;
+    }
+    return check_launch("k_cycle_dcgs2");
+}
+
 template <typename T> int run_cycle(const mpk_cycle_desc *d, cudaStream_t s) {
     const int64_t n = d->n, ld = d->ld;
     const int m = d->m;
@@ -738,6 +797,13 @@ template <typename T> int run_cycle(const mpk_cycle_desc *d, cudaStream_t s) {
     // register kernel applies it inside its SpMV input and correction
     const bool diag1 = precond && d->M->kind == MPK_PC_JACOBI && d->M->block == 1 && d->M->n == n &&
                        d->M->dtype == d->dtype;
+    // fp64 only: in fp32 the lagged (Pythagorean) norm loses its digits near
+    // the cycle's attainable accuracy; fp32 cycles keep CGS2
+    if ((d->flags & 16) && sizeof(T) == 8 && !precond && d->nranks <= 1 && m + 1 <= kRegMaxCols &&
+        (uintptr_t)d->x_out % 16 == 0 &&
+        (uintptr_t)d->V % 16 == 0 && (uintptr_t)d->work % 16 == 0 && (uintptr_t)d->r0 % 16 == 0) {
+        return with_op<T>(d->A, [&](auto op) -> int { return launch_dcgs2<T, decltype(op)>(op, d, cap, tf, u, s); });
+    }
     // identity preconditioner, any m: the persistent register kernel (column
     // blocks beyond 51 columns); MPK_FUSED_IMPL=tma keeps the TMA ring for m <= 63
     if (!precond && !(d->flags & 4) && !fused_use_tma() && (uintptr_t)d->x_out % 16 == 0 &&

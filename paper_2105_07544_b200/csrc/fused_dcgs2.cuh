@@ -1,0 +1,343 @@
+// Persistent cycle kernel with the lagged one-reduction CGS2 ("DCGS2"):
+// mathematically the reference's CGS2 Arnoldi (kernels.py:98-126), reordered
+// so each step needs ONE global reduction and TWO passes over the basis
+// (the reference's form needs 4 passes; k_cycle_reg needs 3 and 3 grid
+// barriers).  Opt-in (SolverConfig.orthogonalization = "dcgs2"); identity
+// preconditioner, m <= 51, one GPU.
+//
+// State entering step j (1..m): Q_j = [q_0..q_{j-1}] (final), u = w_{j-1} -
+// Q_j c (w_{j-1} = A q_{j-1} after its first CGS pass c, neither
+// re-orthogonalised nor normalised).  Step j:
+//   z = A u                                           (SpMV, own rows)
+//   [X0, X1, a, b] = [Q_j^T u, Q_j^T z, u.u, u.z]     (ONE reduction)
+//   rho = sqrt(a - X0.X0)                             (norm of the re-orthogonalised u)
+//   H[:, j-1] = [c + X0; rho]   (= CGS2's c1 + c2 and beta: column j-1 final)
+//   Givens on column j-1, implicit residual of step j, exit test
+//   t = (b - X0.X1)/rho,  tau = t/rho
+//   c' = ([X1; t] - H[:j+1, :j] X0)/rho             (first-pass coefficients of A q_j)
+//   q_j = (u - Q_j X0)/rho,  u' = (z - Q_j (X1 - X0 tau) - u tau)/rho     (ONE update pass)
+// The identities used: A Q_j = Q_{j+1} H (Arnoldi), so A q_j = (z - Q_{j+1} H X0)/rho,
+// and ||w_{j-1}||^2 = ||u||^2 + ||c||^2 for the reference's append test.
+#pragma once
+
+#include "fused_reg.cuh"
+
+namespace mpk {
+
+enum { kDcDots2 = 0, kDcUpdate2 = 1 };
+
+// x accessor of the unnormalised candidate u (complete before the SpMV: every
+// CTA wrote its rows before the last grid barrier)
+template <typename T> struct XCg {
+    const T *p;
+    __device__ __forceinline__ T operator()(int64_t c) const { return __ldcg(p + c); }
+    __device__ __forceinline__ Pack<T> vec(int64_t c) const { return ldcg16(p + c); }
+};
+
+// kDcDots2:   a0[i] += V[:, c].u, a1[i] += V[:, c].z, e0 += u.u, e1 += u.z
+// kDcUpdate2: q = (u - V X0)/rho -> qout ; u' = (z - V Y - u tau)/rho -> u (in place)
+template <typename T, int MODE, int U>
+__device__ __forceinline__ void dc_phase_u(const T *V, int64_t ld, int nc, int64_t rb, int64_t re, T *u, const T *z,
+                                           T *qout, const T *X0, const T *Y, T rho, T tau,
+                                           T (&a0)[RegCfg<T>::KP], T (&a1)[RegCfg<T>::KP], T &e0, T &e1, bool rev) {
+    using C = RegCfg<T>;
+    constexpr int R = C::R;
+    constexpr int KU = C::KP / U;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane % C::G, p = lane / C::G;
+    constexpr int64_t TRIP = (int64_t)C::WR * U;
+    const int64_t b0 = rb + (int64_t)warp * TRIP, step = (int64_t)kFW * TRIP;
+    const int64_t ntrip = (b0 < re) ? (re - b0 + step - 1) / step : 0;
+    for (int64_t t = 0; t < ntrip; ++t) {
+        const int64_t b = b0 + (rev ? ntrip - 1 - t : t) * step;
+        Pack<T> vv[U][KU], uv[U], zv[U];
+#pragma unroll
+        for (int uu = 0; uu < U; ++uu) {
+            const int64_t r = b + (int64_t)(uu * C::G + g) * R;
+            const bool live = r < re;
+#pragma unroll
+            for (int i = 0; i < KU; ++i) {
+                const int c = p + C::P * i;
+                if (c < nc && live) vv[uu][i] = ldcg16(V + (int64_t)c * ld + r);
+                else {
+#pragma unroll
+                    for (int e = 0; e < R; ++e) vv[uu][i].v[e] = T(0);
+                }
+            }
+            // kDcUpdate2 writes u in place from part 0: only part 0 reads it there
+            const bool need = live && (MODE == kDcDots2 || p == 0);
+            if (need) {
+                uv[uu] = ldcg16(u + r);
+                zv[uu] = ldcg16(z + r);
+            } else {
+#pragma unroll
+                for (int e = 0; e < R; ++e) uv[uu].v[e] = zv[uu].v[e] = T(0);
+            }
+        }
+#pragma unroll
+        for (int uu = 0; uu < U; ++uu) {
+            const int64_t r = b + (int64_t)(uu * C::G + g) * R;
+            const bool live = r < re;
+            if (MODE == kDcDots2) {
+#pragma unroll
+                for (int i = 0; i < KU; ++i) {
+                    if (p + C::P * i < nc) {
+#pragma unroll
+                        for (int e = 0; e < R; ++e) {
+                            a0[i] += vv[uu][i].v[e] * uv[uu].v[e];
+                            a1[i] += vv[uu][i].v[e] * zv[uu].v[e];
+                        }
+                    }
+                }
+                if (p == 0) {
+#pragma unroll
+                    for (int e = 0; e < R; ++e) {
+                        e0 += uv[uu].v[e] * uv[uu].v[e];
+                        e1 += uv[uu].v[e] * zv[uu].v[e];
+                    }
+                }
+                continue;
+            }
+            T s1[R], s2[R];
+#pragma unroll
+            for (int e = 0; e < R; ++e) s1[e] = s2[e] = T(0);
+#pragma unroll
+            for (int i = 0; i < KU; ++i) {
+                const int c = p + C::P * i;
+                if (c < nc) {
+                    const T c1 = X0[c], c2 = Y[c];
+#pragma unroll
+                    for (int e = 0; e < R; ++e) {
+                        s1[e] += vv[uu][i].v[e] * c1;
+                        s2[e] += vv[uu][i].v[e] * c2;
+                    }
+                }
+            }
+#pragma unroll
+            for (int o = C::G; o < 32; o <<= 1) {
+#pragma unroll
+                for (int e = 0; e < R; ++e) {
+                    s1[e] += __shfl_xor_sync(0xffffffffu, s1[e], o);
+                    s2[e] += __shfl_xor_sync(0xffffffffu, s2[e], o);
+                }
+            }
+            if (p == 0 && live) {
+                Pack<T> qv, un;
+#pragma unroll
+                for (int e = 0; e < R; ++e) {
+                    qv.v[e] = RN<T>::div(RN<T>::sub(uv[uu].v[e], s1[e]), rho);
+                    un.v[e] = RN<T>::div(RN<T>::sub(RN<T>::sub(zv[uu].v[e], s2[e]), RN<T>::mul(uv[uu].v[e], tau)), rho);
+                }
+                stcg16(qout + r, qv);
+                stcg16(u + r, un);
+            }
+        }
+    }
+}
+
+template <typename T, int MODE>
+__device__ __forceinline__ void dc_phase(const T *V, int64_t ld, int nc, int64_t rb, int64_t re, T *u, const T *z,
+                                         T *qout, const T *X0, const T *Y, T rho, T tau, T (&a0)[RegCfg<T>::KP],
+                                         T (&a1)[RegCfg<T>::KP], T &e0, T &e1, bool rev) {
+    using C = RegCfg<T>;
+    const int ncp = (nc + C::P - 1) / C::P;
+    if (ncp * 4 <= C::KP) dc_phase_u<T, MODE, 4>(V, ld, nc, rb, re, u, z, qout, X0, Y, rho, tau, a0, a1, e0, e1, rev);
+    else if (ncp * 2 <= C::KP) dc_phase_u<T, MODE, 2>(V, ld, nc, rb, re, u, z, qout, X0, Y, rho, tau, a0, a1, e0, e1, rev);
+    else dc_phase_u<T, MODE, 1>(V, ld, nc, rb, re, u, z, qout, X0, Y, rho, tau, a0, a1, e0, e1, rev);
+}
+
+// SpMV of the candidate: y = A x over the CTA's rows, x read through L2.
+template <typename T, class Op>
+__device__ __noinline__ void dc_spmv(const Op &A, const T *x, T *y, int64_t rb, int64_t re, T *sstage) {
+    const XCg<T> xs{x};
+    if constexpr (!Op::kStencil) {
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        T *sb = sstage + warp * kCsrWarpBuf;
+        for (int64_t r0 = rb + (int64_t)warp * 32; r0 < re; r0 += (int64_t)kFW * 32) {
+            const T yr = A.template warp_rows<8>(r0, re, xs, sb);
+            if (r0 + lane < re) y[r0 + lane] = yr;
+        }
+    } else if (A.group_ok()) {
+        constexpr int R = RegCfg<T>::R;
+        auto xv = [&](int64_t c) { return xs.vec(c); };
+        for (int64_t r = rb + (int64_t)threadIdx.x * R; r < re; r += (int64_t)kFB * R) {
+            Pack<T> o;
+            A.row_group(r, xv, xs, o.v);
+            stcg16(y + r, o);
+        }
+    } else {
+        for (int64_t r = rb + threadIdx.x; r < re; r += kFB) y[r] = A.row(r, xs);
+    }
+}
+
+template <typename T, class Op>
+__global__ void __launch_bounds__(kFB, 1) k_cycle_dcgs2(Op A, FusedArgs<T> a) {
+    using C = RegCfg<T>;
+    extern __shared__ __align__(16) unsigned char dsm_dc[];
+    const int m = a.m, ldr = m + 1;
+    T *sR = reinterpret_cast<T *>(dsm_dc);     // (m+1) x m rotated columns
+    T *sH = sR + (int64_t)ldr * m;             // (m+1) x m raw columns (c + X0, rho)
+    T *scs = sH + (int64_t)ldr * m;
+    T *ssn = scs + m;
+    T *sg = ssn + m;                           // m + 1
+    T *sX0 = sg + (m + 1);                     // 64 (+ a at [63])
+    T *sX1 = sX0 + 64;                         // 64 (+ b at [63])
+    T *sc = sX1 + 64;                          // 64: first-pass coefficients of the candidate
+    T *sY = sc + 64;                           // 64
+    T *scol = sY + 64;                         // 64: column being rotated
+    T *sred = scol + 64;                       // kFW * kFSlots
+    T *sstage = sred + kFW * kFSlots;          // kFW * kCsrWarpBuf
+    __shared__ T s_gamma, s_rho, s_tau, s_beta;
+    __shared__ int s_done, s_steps, s_break, s_app;
+    __shared__ double s_scale;
+
+    const int tid = threadIdx.x;
+    const unsigned nb = gridDim.x;
+    const int64_t rpc = ((a.n + nb - 1) / nb + 63) / 64 * 64;
+    const int64_t rb = (int64_t)blockIdx.x * rpc;
+    const int64_t re = (rb + rpc < a.n) ? rb + rpc : a.n;
+    const bool lead = (blockIdx.x == 0);
+    // partial slots (stride kFMaxCtas): X0 -> [0, 52), a -> 104, X1 -> [52, 104), b -> 105
+    constexpr int kSlotB = 52, kXa = 104, kXb = 105, kDcSlots = 106;
+    T *part = a.part, *partC = a.part + (int64_t)kDcSlots * kFMaxCtas;
+    T *u = a.w, *z = a.wp;
+
+    if (tid == 0) {
+        const T gamma = RN<T>::sqrt_(__ldcg(a.rnorm2));
+        s_gamma = gamma;
+        double scale = a.norm_scale > 0.0 ? a.norm_scale : (double)gamma;
+        if (gamma == T(0) && !(scale > 0.0)) scale = 1.0;   // gmres.py:170-172
+        s_scale = scale;
+        s_done = (gamma == T(0)) ? 1 : 0;
+        s_steps = 0;
+        s_break = 0;
+        sg[0] = gamma;
+        if (lead) {
+            a.ctl->gamma = (double)gamma;
+            a.ctl->scale = scale;
+            a.ctl->steps = 0;
+            a.ctl->breakdown = 0;
+            a.ctl->tri_err = 0;
+            a.ctl->pad_ = 0;
+            a.ctl->done = s_done;
+            a.H.g[0] = gamma;
+        }
+    }
+    __syncthreads();
+    T a0[C::KP], a1[C::KP];
+    if (!s_done) {
+        // ---- prologue: q_0 = r0/gamma ; w = A q_0 ; c = q_0.w ; u = w - q_0 c
+        const T gm = s_gamma;
+        T *q0 = a.V;
+        for (int64_t r = rb + tid; r < re; r += kFB) q0[r] = RN<T>::div(__ldcg(a.r0 + r), gm);
+        __syncthreads();
+        phase_a_spmv<T>(A, XSlab<T>{a.r0, q0, gm, rb, re, nullptr, nullptr}, z, rb, re, sstage);
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < C::KP; ++i) a0[i] = T(0);
+        T ext = T(0);
+        reg_phase<T, kRegDots>(a.V, a.ld, 1, rb, re, a.n, z, nullptr, nullptr, a0, ext);
+        reg_write_partials<T>(a0, 1, T(0), sred, part, nullptr, 0, 0, false, kXa);
+        grid_sync(a.bar, nb);
+        cross_reduce<T>(part, nb, 1, 1, sc, kFMaxCtas, kXa);   // sc[0] = c
+        __syncthreads();
+        reg_phase<T, kRegUpdateNorm>(a.V, a.ld, 1, rb, re, a.n, z, u, sc, a0, ext);   // u = w - q_0 c
+        grid_sync(a.bar, nb);
+    }
+    // ---- steps j = 1..cap: finalise column j-1, build q_j and the next candidate
+    for (int j = 1; j <= a.cap && !s_done; ++j) {
+        dc_spmv<T>(A, u, z, rb, re, sstage);   // z = A u
+        __syncthreads();
+        T e0 = T(0), e1 = T(0);
+#pragma unroll
+        for (int i = 0; i < C::KP; ++i) a0[i] = a1[i] = T(0);
+        dc_phase<T, kDcDots2>(a.V, a.ld, j, rb, re, u, z, nullptr, nullptr, nullptr, T(0), T(0), a0, a1, e0, e1,
+                              j & 1);
+        reg_write_partials<T>(a0, j, e0, sred, part, nullptr, 0, 0, true, kXa);
+        reg_write_partials<T>(a1, j, e1, sred, part, nullptr, 0, kSlotB, true, kXb);
+        grid_sync(a.bar, nb);
+        cross_reduce<T>(part, nb, j, j, sX0, kFMaxCtas, kXa);                                    // X0
+        cross_reduce<T>(part + (int64_t)kSlotB * kFMaxCtas, nb, j, j, sX1, kFMaxCtas, kXb - kSlotB);   // X1
+        cross_reduce<T>(part, nb, 0, 1, sX0 + 63, kFMaxCtas, kXa);                               // a
+        cross_reduce<T>(part, nb, 0, 1, sX1 + 63, kFMaxCtas, kXb);                               // b
+        __syncthreads();
+        // ---- column j-1 (every CTA, identical): H[:, j-1] = [c + X0; rho]
+        const int k = j - 1, nc = j;
+        if (tid == 0) {
+            T x0x0 = T(0), cc = T(0), x0x1 = T(0);
+            for (int i = 0; i < j; ++i) {
+                x0x0 += sX0[i] * sX0[i];
+                cc += sc[i] * sc[i];
+                x0x1 += sX0[i] * sX1[i];
+            }
+            const T av = sX0[63], bv = sX1[63];
+            T rho2 = RN<T>::sub(av, x0x0);
+            // the Pythagorean norm is only trusted while it keeps ~2 digits
+            // (rho^2 >= eta * ||u||^2, eta ~ 100 u / 1e-2); below that u is
+            // (numerically) inside span(Q_j): treated as the reference's
+            // lucky breakdown (beta = 0, kernels.py:122-126), which ends the
+            // cycle with column j-1 included
+            const T eta = sizeof(T) == 4 ? T(1e-3) : T(1e-11);
+            if (!(rho2 > eta * av)) rho2 = T(0);
+            const T rho = RN<T>::sqrt_(rho2);
+            s_rho = rho;
+            const T t = RN<T>::div(RN<T>::sub(bv, x0x1), rho);
+            s_tau = RN<T>::div(t, rho);
+            sX1[j] = t;   // [X1; t]
+            // the reference's append test uses ||w_{j-1}||^2 = ||u||^2 + ||c||^2
+            sY[63] = RN<T>::add(av, cc);
+            sY[62] = rho2;
+        }
+        __syncthreads();
+        for (int i = tid; i < nc; i += kFB) {
+            const T hv = RN<T>::add(sc[i], sX0[i]);
+            sH[(int64_t)k * ldr + i] = hv;
+            scol[i] = hv;
+        }
+        if (tid == 0) {
+            sH[(int64_t)k * ldr + nc] = s_rho;
+        }
+        __syncthreads();
+        if (tid == 0)
+            givens_step<T>(a, k, nc, ldr, scol, sY[62], sY[63], s_scale, lead, scs, ssn, sg, s_beta, s_steps,
+                           s_done, s_break);
+        __syncthreads();
+        for (int i = tid; i <= nc; i += kFB) sR[(int64_t)k * ldr + i] = scol[i];
+        if (s_done) break;
+        // ---- next candidate: c' = ([X1; t] - H[:j+1, :j] X0)/rho ; Y = X1 - X0 tau
+        const T rho = s_rho, tau = s_tau;
+        for (int i = tid; i <= j; i += kFB) {
+            T hs = T(0);
+            for (int l = 0; l < j; ++l) hs += sH[(int64_t)l * ldr + i] * sX0[l];   // H[i, l], l <= j-1
+            sc[i] = RN<T>::div(RN<T>::sub(sX1[i], hs), rho);
+        }
+        for (int i = tid; i < j; i += kFB) sY[i] = RN<T>::sub(sX1[i], RN<T>::mul(sX0[i], tau));
+        __syncthreads();
+        // ---- one update pass: q_j -> V[:, j], candidate u' in place
+        T e0d = T(0), e1d = T(0);
+        dc_phase<T, kDcUpdate2>(a.V, a.ld, j, rb, re, u, z, a.V + (int64_t)j * a.ld, sX0, sY, rho, tau, a0, a1, e0d,
+                                e1d, (j + 1) & 1);
+        grid_sync(a.bar, nb);
+    }
+
+    // ---------------- epilogue: d = R \ g, x_out = x0 + V_k d
+    const int k = s_steps;
+    T *sd = sc;
+    if (k > 0 && tid < 32) back_substitute<T>(a, k, ldr, sR, sg, sY, sd, lead, s_app);
+    __syncthreads();
+    if (k > 0 && s_app) return;   // TriangularBreakdownError: x_out untouched
+    if (lead) {
+        for (int i = tid; i < k; i += kFB) a.H.d[i] = sd[i];
+        for (int i = tid; i < k * ldr; i += kFB) a.H.h[i] = sR[i];
+        for (int i = tid; i <= k; i += kFB) a.H.g[i] = sg[i];
+    }
+    if (k == 0) {
+        for (int64_t r = rb + tid; r < re; r += kFB) a.x_out[r] = a.x0[r];
+        return;
+    }
+    T ext = T(0);
+    reg_phase<T, kRegCorrect>(a.V, a.ld, k, rb, re, a.n, a.x0, a.x_out, sd, a0, ext);
+    (void)partC;
+}
+
+}  // namespace mpk

@@ -96,7 +96,7 @@ class CycleWorkspace:
     def clear_changed(self):
         self.ctlbuf[OFF_CHANGED:OFF_CHANGED + 4].zero_()
 
-    def cycle(self, A, M, r0, rnorm2_off, x0, x_out, steps_cap, exit_tol, norm_scale, rule):
+    def cycle(self, A, M, r0, rnorm2_off, x0, x_out, steps_cap, exit_tol, norm_scale, rule, orth="cgs2"):
         """Enqueue one whole cycle (gmres.py:134-205) via mpk_cycle_run."""
         d = self.desc
         self._pins = [A.descriptor()]
@@ -125,7 +125,7 @@ class CycleWorkspace:
         d.ws = self.ws.ptr
         d.ctl = self.ctl_ptr
         d.nranks = 1
-        d.flags = self.flags
+        d.flags = self.flags | (16 if orth == "dcgs2" else 0)
         _lib.check(D.lib().mpk_cycle_run(ctypes.byref(d), D.stream()))
 
     # -- readback -----------------------------------------------------------
