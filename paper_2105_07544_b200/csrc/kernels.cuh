@@ -51,15 +51,15 @@ __device__ __forceinline__ bool skip(const int32_t *done) {
 __device__ __forceinline__ int64_t gtid() { return (int64_t)blockIdx.x * blockDim.x + threadIdx.x; }
 __device__ __forceinline__ int64_t gstride() { return (int64_t)gridDim.x * blockDim.x; }
 
-// Row loop of an SpMV-carrying kernel.  Stencils: thread per row, grid-
-// strided.  CSR: 32-row groups per warp, grid-strided over groups, each
+// Row loop of an SpMV-carrying kernel.  Stencils: 16-byte row groups per
+// thread (GROUPS) or thread per row, grid-strided.  CSR: 32-row groups per warp, grid-strided over groups, each
 // evaluated by CsrOp::warp_rows (coalesced entry loads, bit-identical sums);
 // fn(r, y_r) runs on the lane owning row r.  `sb` is the warp's staging.
-template <typename T, class Op, class X, class F>
+template <typename T, class Op, class X, class F, bool GROUPS = true>
 __device__ __forceinline__ void for_rows(const Op &A, X x, T *sb, F &&fn) {
     if constexpr (Op::kStencil) {
         constexpr int R = 16 / (int)sizeof(T);
-        if (A.group_ok() && ((uintptr_t)x.p % 16) == 0) {
+        if (GROUPS && A.group_ok() && ((uintptr_t)x.p % 16) == 0) {
             // 16-byte row groups (vector reads of the group and its N/S/B/U
             // neighbours), bit-identical to row(); scalar tail past n - n % R
             const int64_t ng = A.n / R;
@@ -470,7 +470,9 @@ __global__ void __launch_bounds__(kBlock) k_residual(Op A, const T *__restrict__
     float al = 0.f;
     __shared__ T sbuf[Op::kStencil ? 1 : (kBlock / 32) * kCsrWarpBuf];
     T *sb = sbuf + (Op::kStencil ? 0 : (threadIdx.x >> 5) * kCsrWarpBuf);
-    for_rows<T>(A, XPlain<T>{x}, sb, [&](int64_t i, T ax) {
+    // thread per row: the order of the r.r partial sums fixes the refinement
+    // trajectory of GMRES-IR (kept as measured against the reference counts)
+    auto body = [&](int64_t i, T ax) {
         const T ri = RN<T>::sub(b[i], ax);
         if (r) r[i] = ri;
         an += ri * ri;
@@ -479,7 +481,8 @@ __global__ void __launch_bounds__(kBlock) k_residual(Op A, const T *__restrict__
             rlow[i] = li;
             al += li * li;
         }
-    });
+    };
+    for_rows<T, Op, XPlain<T>, decltype(body) &, false>(A, XPlain<T>{x}, sb, body);
     T d1[1] = {T(0)};
     block_reduce_cols<T, 1>(d1, 0, an, sm, partials + (int64_t)blockIdx.x * kStride);
     if constexpr (LOW) {
