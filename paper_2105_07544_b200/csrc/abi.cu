@@ -797,9 +797,7 @@ template <typename T> int run_cycle(const mpk_cycle_desc *d, cudaStream_t s) {
     // register kernel applies it inside its SpMV input and correction
     const bool diag1 = precond && d->M->kind == MPK_PC_JACOBI && d->M->block == 1 && d->M->n == n &&
                        d->M->dtype == d->dtype;
-    // fp64 only: in fp32 the lagged (Pythagorean) norm loses its digits near
-    // the cycle's attainable accuracy; fp32 cycles keep CGS2
-    if ((d->flags & 16) && sizeof(T) == 8 && !precond && d->nranks <= 1 && m + 1 <= kRegMaxCols &&
+    if ((d->flags & 16) && !precond && d->nranks <= 1 && m + 1 <= kRegMaxCols &&
         (uintptr_t)d->x_out % 16 == 0 &&
         (uintptr_t)d->V % 16 == 0 && (uintptr_t)d->work % 16 == 0 && (uintptr_t)d->r0 % 16 == 0) {
         return with_op<T>(d->A, [&](auto op) -> int { return launch_dcgs2<T, decltype(op)>(op, d, cap, tf, u, s); });

@@ -308,7 +308,8 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_dcgs2(Op A, FusedArgs<T> a) {
         const T rho = s_rho, tau = s_tau;
         for (int i = tid; i <= j; i += kFB) {
             T hs = T(0);
-            for (int l = 0; l < j; ++l) hs += sH[(int64_t)l * ldr + i] * sX0[l];   // H[i, l], l <= j-1
+            // Hessenberg: H[i, l] = 0 below the subdiagonal (l < i - 1; never stored)
+            for (int l = (i > 0 ? i - 1 : 0); l < j; ++l) hs += sH[(int64_t)l * ldr + i] * sX0[l];
             sc[i] = RN<T>::div(RN<T>::sub(sX1[i], hs), rho);
         }
         for (int i = tid; i < j; i += kFB) sY[i] = RN<T>::sub(sX1[i], RN<T>::mul(sX0[i], tau));

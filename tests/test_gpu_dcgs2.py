@@ -1,6 +1,6 @@
 """The lagged one-reduction CGS2 cycle (SolverConfig.orthogonalization =
 "dcgs2") is the reference's CGS2 Arnoldi reordered (fused_dcgs2.cuh): same
-Hessenberg in exact arithmetic.  binary64 only (fp32 cycles keep CGS2).  Bars: implicit-residual histories of one
+Hessenberg in exact arithmetic.  Bars: implicit-residual histories of one
 cycle agree with the CGS2 kernel to rounding, restarted / IR solves converge
 to 1e-10 with iteration counts within one restart cycle of CGS2's (equal on
 the reference goldens that have margin)."""
@@ -20,16 +20,18 @@ def L(preset, nx):
 
 @pytest.mark.parametrize("preset,nx,prec,tol", [("BentPipe2D", 64, P.binary64, 1e-8),
                                                  ("Laplace3D", 16, P.binary64, 1e-8),
-                                                 ("UniFlow2D", 48, P.binary64, 1e-8)])
+                                                 ("UniFlow2D", 48, P.binary64, 1e-8),
+                                                 ("BentPipe2D", 64, P.binary32, 2e-3)])
 def test_one_cycle_history_matches_cgs2(cuda, preset, nx, prec, tol):
     A = mk.convert_matrix(L(preset, nx), prec)
     b = np.ones(A.n, prec.dtype)
-    cfg = dict(m=40, rtol=1e-300, precision=prec, breakdown_rule="u")
+    # fp32: exit at 1e-5, above the cycle's attainable accuracy
+    cfg = dict(m=40, rtol=1e-300 if prec is P.binary64 else 1e-5, precision=prec, breakdown_rule="u")
     x1, s1 = mk.gmres_cycle(A, None, b, np.zeros(A.n, prec.dtype), mk.SolverConfig(**cfg))
     x2, s2 = mk.gmres_cycle(A, None, b, np.zeros(A.n, prec.dtype), mk.SolverConfig(orthogonalization="dcgs2", **cfg))
     assert s1.steps == s2.steps
     h1, h2 = np.array(s1.implicit_relres), np.array(s2.implicit_relres)
-    keep = h1 > (1e-12 if prec is P.binary64 else 1e-5)
+    keep = h1 > (1e-12 if prec is P.binary64 else 1e-4)
     assert np.all(np.abs(h1 - h2)[keep] <= tol * h1[keep]), np.max(np.abs(h1 - h2)[keep] / h1[keep])
     assert np.abs(x1 - x2).max() <= (1e-9 if prec is P.binary64 else 1e-3) * np.abs(x1).max()
 
@@ -45,13 +47,15 @@ def test_restarted_counts(cuda, runs):
         assert abs(rep.total_iters - g["iters"]) <= 50, (name, rep.total_iters, g["iters"])
 
 
-def test_fp32_requests_fall_back_to_cgs2(cuda):
-    A = L("BentPipe2D", 64)
-    reps = []
-    for orth in ("cgs2", "dcgs2"):
-        inner = mk.SolverConfig(m=50, rtol=1e-4, precision=P.binary32, orthogonalization=orth)
-        reps.append(mk.gmres_ir(A, np.ones(A.n), np.zeros(A.n), mk.IrConfig(inner=inner, rtol=1e-10)))
-    assert reps[0].total_iters == reps[1].total_iters and reps[0].x.tobytes() == reps[1].x.tobytes()
+def test_ir_converges_like_cgs2(cuda):
+    for preset, nx in (("BentPipe2D", 96), ("Laplace3D", 24)):
+        A = L(preset, nx)
+        reps = []
+        for orth in ("cgs2", "dcgs2"):
+            inner = mk.SolverConfig(m=50, rtol=1e-4, precision=P.binary32, orthogonalization=orth, max_iters=20000)
+            reps.append(mk.gmres_ir(A, np.ones(A.n), np.zeros(A.n), mk.IrConfig(inner=inner, rtol=1e-10)))
+        assert all(r.converged and r.final_explicit_relres <= 1e-10 for r in reps)
+        assert abs(reps[0].total_iters - reps[1].total_iters) <= 50, (reps[0].total_iters, reps[1].total_iters)
 
 
 def test_lucky_breakdown_detected(cuda):
