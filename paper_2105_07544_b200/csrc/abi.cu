@@ -620,6 +620,36 @@ int fused_grid(int sms, int64_t n) {
     return g < sms ? (int)g : sms;
 }
 
+// Row-partitioned cycles: the rank's view of the communicator into the
+// kernel arguments (w'' / the candidate live in the rank's global-length x
+// buffer); the CTA count is the communicator's (all ranks must agree).
+template <typename T> int fill_comm(FusedArgs<T> &fa, const mpk_cycle_desc *d, int &grid) {
+    memset(&fa.cm, 0, sizeof(fa.cm));
+    fa.cm.nranks = 1;
+    if (d->nranks > 1) {
+        const mpk_comm *c = d->comm;
+        if (!c || c->nranks != d->nranks || c->nranks > kMaxRanks || c->rank < 0 || c->rank >= c->nranks)
+            return fail(MPK_EARG, "multi-rank cycle needs a consistent mpk_comm");
+        fa.cm.rank = c->rank;
+        fa.cm.nranks = c->nranks;
+        fa.cm.row0 = c->row0;
+        fa.cm.epoch = (unsigned long long *)c->epoch;
+        for (int q = 0; q < c->nranks; ++q) {
+            fa.cm.part[q] = (T *)c->part[q];
+            fa.cm.xbar[q] = (unsigned long long *)c->xbar[q];
+            fa.cm.xg[q] = (T *)c->xg[q];
+            fa.cm.mir_lo[q] = c->mir_lo[q];
+            fa.cm.mir_hi[q] = c->mir_hi[q];
+            if (!fa.cm.part[q] || !fa.cm.xbar[q] || !fa.cm.xg[q]) return fail(MPK_EARG, "null peer pointer");
+        }
+        if (c->row0 % 64 != 0 || ((uintptr_t)c->xg[c->rank] % 16) != 0)
+            return fail(MPK_EARG, "rank row blocks must start on 64-row boundaries");
+        fa.wpp = (T *)c->xg[c->rank] + c->row0;   // w'' lives in the rank's global-length vector
+        if (c->ctas > 0 && c->ctas < grid) grid = c->ctas;
+    }
+    return MPK_OK;
+}
+
 template <typename T, class Op>
 int launch_fused_reg(const Op &op, const mpk_cycle_desc *d, int cap, double tf, double u, cudaStream_t s) {
     const int m = d->m;
@@ -673,29 +703,7 @@ int launch_fused_reg(const Op &op, const mpk_cycle_desc *d, int cap, double tf, 
     fa.z = w + 3 * d->ld;
     if (d->M && d->M->kind == MPK_PC_JACOBI && d->M->block == 1 && d->M->dtype == d->dtype)
         fa.diag = (const T *)d->M->lu;
-    memset(&fa.cm, 0, sizeof(fa.cm));
-    fa.cm.nranks = 1;
-    if (d->nranks > 1) {
-        const mpk_comm *c = d->comm;
-        if (!c || c->nranks != d->nranks || c->nranks > kMaxRanks || c->rank < 0 || c->rank >= c->nranks)
-            return fail(MPK_EARG, "multi-rank cycle needs a consistent mpk_comm");
-        fa.cm.rank = c->rank;
-        fa.cm.nranks = c->nranks;
-        fa.cm.row0 = c->row0;
-        fa.cm.epoch = (unsigned long long *)c->epoch;
-        for (int q = 0; q < c->nranks; ++q) {
-            fa.cm.part[q] = (T *)c->part[q];
-            fa.cm.xbar[q] = (unsigned long long *)c->xbar[q];
-            fa.cm.xg[q] = (T *)c->xg[q];
-            fa.cm.mir_lo[q] = c->mir_lo[q];
-            fa.cm.mir_hi[q] = c->mir_hi[q];
-            if (!fa.cm.part[q] || !fa.cm.xbar[q] || !fa.cm.xg[q]) return fail(MPK_EARG, "null peer pointer");
-        }
-        if (c->row0 % 64 != 0 || ((uintptr_t)c->xg[c->rank] % 16) != 0)
-            return fail(MPK_EARG, "rank row blocks must start on 64-row boundaries");
-        fa.wpp = (T *)c->xg[c->rank] + c->row0;   // w'' lives in the rank's global-length vector
-        if (c->ctas > 0 && c->ctas < grid) grid = c->ctas;
-    }
+    if (int rc = fill_comm<T>(fa, d, grid)) return rc;
     Op opc = op;
     void *args[] = {(void *)&opc, (void *)&fa};
     ProfScope ps(7, 0.0, s);
@@ -731,7 +739,7 @@ int launch_dcgs2(const Op &op, const mpk_cycle_desc *d, int cap, double tf, doub
     if (per_sm < 1) return fail(MPK_ELAUNCH, "dcgs2 cycle kernel does not fit on an SM");
     int grid = sm_count_cached();
     if (grid > 160) grid = 160;   // cross_reduce fast path
-    grid = fused_grid(grid, d->n);
+    if (d->nranks <= 1) grid = fused_grid(grid, d->n);
     FusedArgs<T> fa;
     memset(&fa, 0, sizeof(fa));
     fa.n = d->n;
@@ -754,7 +762,7 @@ int launch_dcgs2(const Op &op, const mpk_cycle_desc *d, int cap, double tf, doub
     fa.exit_tol = d->exit_tol;
     fa.norm_scale = d->norm_scale;
     fa.u = u;
-    fa.cm.nranks = 1;
+    if (int rc = fill_comm<T>(fa, d, grid)) return rc;
     Op opc = op;
     void *args[] = {(void *)&opc, (void *)&fa};
     ProfScope ps(7, 0.0, s);
@@ -797,7 +805,7 @@ template <typename T> int run_cycle(const mpk_cycle_desc *d, cudaStream_t s) {
     // register kernel applies it inside its SpMV input and correction
     const bool diag1 = precond && d->M->kind == MPK_PC_JACOBI && d->M->block == 1 && d->M->n == n &&
                        d->M->dtype == d->dtype;
-    if ((d->flags & 16) && !precond && d->nranks <= 1 && m + 1 <= kRegMaxCols &&
+    if ((d->flags & 16) && !precond && m + 1 <= kRegMaxCols &&
         (uintptr_t)d->x_out % 16 == 0 &&
         (uintptr_t)d->V % 16 == 0 && (uintptr_t)d->work % 16 == 0 && (uintptr_t)d->r0 % 16 == 0) {
         return with_op<T>(d->A, [&](auto op) -> int { return launch_dcgs2<T, decltype(op)>(op, d, cap, tf, u, s); });

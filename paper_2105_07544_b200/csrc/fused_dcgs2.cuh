@@ -39,7 +39,8 @@ template <typename T> struct XCg {
 template <typename T, int MODE, int U>
 __device__ __forceinline__ void dc_phase_u(const T *V, int64_t ld, int nc, int64_t rb, int64_t re, T *u, const T *z,
                                            T *qout, const T *X0, const T *Y, T rho, T tau,
-                                           T (&a0)[RegCfg<T>::KP], T (&a1)[RegCfg<T>::KP], T &e0, T &e1, bool rev) {
+                                           T (&a0)[RegCfg<T>::KP], T (&a1)[RegCfg<T>::KP], T &e0, T &e1, bool rev,
+                                           const CommArgs<T> *cm) {
     using C = RegCfg<T>;
     constexpr int R = C::R;
     constexpr int KU = C::KP / U;
@@ -130,6 +131,11 @@ __device__ __forceinline__ void dc_phase_u(const T *V, int64_t ld, int nc, int64
                 }
                 stcg16(qout + r, qv);
                 stcg16(u + r, un);
+                if (cm != nullptr) {   // halo rows of the candidate for the other ranks' SpMV (P2P)
+                    for (int q = 0; q < cm->nranks; ++q)
+                        if (q != cm->rank && r >= cm->mir_lo[q] && r < cm->mir_hi[q])
+                            stcg16(cm->xg[q] + cm->row0 + r, un);
+                }
             }
         }
     }
@@ -138,12 +144,12 @@ __device__ __forceinline__ void dc_phase_u(const T *V, int64_t ld, int nc, int64
 template <typename T, int MODE>
 __device__ __forceinline__ void dc_phase(const T *V, int64_t ld, int nc, int64_t rb, int64_t re, T *u, const T *z,
                                          T *qout, const T *X0, const T *Y, T rho, T tau, T (&a0)[RegCfg<T>::KP],
-                                         T (&a1)[RegCfg<T>::KP], T &e0, T &e1, bool rev) {
+                                         T (&a1)[RegCfg<T>::KP], T &e0, T &e1, bool rev, const CommArgs<T> *cm) {
     using C = RegCfg<T>;
     const int ncp = (nc + C::P - 1) / C::P;
-    if (ncp * 4 <= C::KP) dc_phase_u<T, MODE, 4>(V, ld, nc, rb, re, u, z, qout, X0, Y, rho, tau, a0, a1, e0, e1, rev);
-    else if (ncp * 2 <= C::KP) dc_phase_u<T, MODE, 2>(V, ld, nc, rb, re, u, z, qout, X0, Y, rho, tau, a0, a1, e0, e1, rev);
-    else dc_phase_u<T, MODE, 1>(V, ld, nc, rb, re, u, z, qout, X0, Y, rho, tau, a0, a1, e0, e1, rev);
+    if (ncp * 4 <= C::KP) dc_phase_u<T, MODE, 4>(V, ld, nc, rb, re, u, z, qout, X0, Y, rho, tau, a0, a1, e0, e1, rev, cm);
+    else if (ncp * 2 <= C::KP) dc_phase_u<T, MODE, 2>(V, ld, nc, rb, re, u, z, qout, X0, Y, rho, tau, a0, a1, e0, e1, rev, cm);
+    else dc_phase_u<T, MODE, 1>(V, ld, nc, rb, re, u, z, qout, X0, Y, rho, tau, a0, a1, e0, e1, rev, cm);
 }
 
 // SpMV of the candidate: y = A x over the CTA's rows, x read through L2.
@@ -197,10 +203,35 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_dcgs2(Op A, FusedArgs<T> a) {
     const int64_t rb = (int64_t)blockIdx.x * rpc;
     const int64_t re = (rb + rpc < a.n) ? rb + rpc : a.n;
     const bool lead = (blockIdx.x == 0);
-    // partial slots (stride kFMaxCtas): X0 -> [0, 52), a -> 104, X1 -> [52, 104), b -> 105
-    constexpr int kSlotB = 52, kXa = 104, kXb = 105, kDcSlots = 106;
-    T *part = a.part, *partC = a.part + (int64_t)kDcSlots * kFMaxCtas;
-    T *u = a.w, *z = a.wp;
+    // partial slots: X0 -> [0, 52), a -> 104, X1 -> [52, 104), b -> 105.
+    // Row-partitioned (nranks > 1): every rank's buffer, columns rank * nb + cta,
+    // the candidate u lives in the rank's global-length x buffer (halo rows
+    // mirrored P2P by the neighbours), barriers span all ranks.
+    constexpr int kSlotB = 52, kXa = 104, kXb = 105;
+    const bool multi = a.cm.nranks > 1;
+    const CommArgs<T> *cmp = multi ? &a.cm : nullptr;
+    const int pstride = multi ? kXStride : kFMaxCtas;
+    const unsigned ncol = multi ? nb * (unsigned)a.cm.nranks : nb;
+    T *part = multi ? a.cm.part[a.cm.rank] : a.part;
+    T *u = multi ? a.wpp : a.w, *z = a.wp;
+    unsigned long long ep = multi ? __ldcg(a.cm.epoch) : 0ull;
+    auto sync_all = [&]() -> bool {
+        if (!multi) {
+            grid_sync(a.bar, nb);
+            return false;
+        }
+        ++ep;
+        return grid_sync_x<T>(a.bar, nb, a.cm, ep);
+    };
+    auto finish = [&]() {
+        if (multi && lead && tid == 0) *a.cm.epoch = ep;
+    };
+#define MPK_DC_SYNC()                              \
+    if (sync_all()) {                              \
+        if (lead && tid == 0) a.ctl->pad_ = 1;     \
+        finish();                                  \
+        return;                                    \
+    }
 
     if (tid == 0) {
         const T gamma = RN<T>::sqrt_(__ldcg(a.rnorm2));
@@ -229,20 +260,32 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_dcgs2(Op A, FusedArgs<T> a) {
         // ---- prologue: q_0 = r0/gamma ; w = A q_0 ; c = q_0.w ; u = w - q_0 c
         const T gm = s_gamma;
         T *q0 = a.V;
-        for (int64_t r = rb + tid; r < re; r += kFB) q0[r] = RN<T>::div(__ldcg(a.r0 + r), gm);
+        const T *src = a.r0;
+        if (multi) {
+            // q_0's SpMV reads halo rows of r0: stage r0 in the x buffer, mirror
+            for (int64_t r = rb + tid; r < re; r += kFB) {
+                const T v = a.r0[r];
+                u[r] = v;
+                for (int q = 0; q < a.cm.nranks; ++q)
+                    if (q != a.cm.rank && r >= a.cm.mir_lo[q] && r < a.cm.mir_hi[q]) a.cm.xg[q][a.cm.row0 + r] = v;
+            }
+            src = u;
+            MPK_DC_SYNC();
+        }
+        for (int64_t r = rb + tid; r < re; r += kFB) q0[r] = RN<T>::div(__ldcg(src + r), gm);
         __syncthreads();
-        phase_a_spmv<T>(A, XSlab<T>{a.r0, q0, gm, rb, re, nullptr, nullptr}, z, rb, re, sstage);
+        phase_a_spmv<T>(A, XSlab<T>{src, q0, gm, rb, re, nullptr, nullptr}, z, rb, re, sstage);
         __syncthreads();
 #pragma unroll
         for (int i = 0; i < C::KP; ++i) a0[i] = T(0);
         T ext = T(0);
         reg_phase<T, kRegDots>(a.V, a.ld, 1, rb, re, a.n, z, nullptr, nullptr, a0, ext);
-        reg_write_partials<T>(a0, 1, T(0), sred, part, nullptr, 0, 0, false, kXa);
-        grid_sync(a.bar, nb);
-        cross_reduce<T>(part, nb, 1, 1, sc, kFMaxCtas, kXa);   // sc[0] = c
+        reg_write_partials<T>(a0, 1, T(0), sred, part, cmp, 0, 0, false, kXa);
+        MPK_DC_SYNC();
+        cross_reduce<T>(part, ncol, 1, 1, sc, pstride, kXa);   // sc[0] = c
         __syncthreads();
-        reg_phase<T, kRegUpdateNorm>(a.V, a.ld, 1, rb, re, a.n, z, u, sc, a0, ext);   // u = w - q_0 c
-        grid_sync(a.bar, nb);
+        reg_phase<T, kRegUpdateNorm>(a.V, a.ld, 1, rb, re, a.n, z, u, sc, a0, ext, cmp);   // u = w - q_0 c
+        MPK_DC_SYNC();
     }
     // ---- steps j = 1..cap: finalise column j-1, build q_j and the next candidate
     for (int j = 1; j <= a.cap && !s_done; ++j) {
@@ -252,14 +295,14 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_dcgs2(Op A, FusedArgs<T> a) {
 #pragma unroll
         for (int i = 0; i < C::KP; ++i) a0[i] = a1[i] = T(0);
         dc_phase<T, kDcDots2>(a.V, a.ld, j, rb, re, u, z, nullptr, nullptr, nullptr, T(0), T(0), a0, a1, e0, e1,
-                              j & 1);
-        reg_write_partials<T>(a0, j, e0, sred, part, nullptr, 0, 0, true, kXa);
-        reg_write_partials<T>(a1, j, e1, sred, part, nullptr, 0, kSlotB, true, kXb);
-        grid_sync(a.bar, nb);
-        cross_reduce<T>(part, nb, j, j, sX0, kFMaxCtas, kXa);                                    // X0
-        cross_reduce<T>(part + (int64_t)kSlotB * kFMaxCtas, nb, j, j, sX1, kFMaxCtas, kXb - kSlotB);   // X1
-        cross_reduce<T>(part, nb, 0, 1, sX0 + 63, kFMaxCtas, kXa);                               // a
-        cross_reduce<T>(part, nb, 0, 1, sX1 + 63, kFMaxCtas, kXb);                               // b
+                              j & 1, nullptr);
+        reg_write_partials<T>(a0, j, e0, sred, part, cmp, 0, 0, true, kXa);
+        reg_write_partials<T>(a1, j, e1, sred, part, cmp, 0, kSlotB, true, kXb);
+        MPK_DC_SYNC();
+        cross_reduce<T>(part, ncol, j, j, sX0, pstride, kXa);                                   // X0
+        cross_reduce<T>(part + (int64_t)kSlotB * pstride, ncol, j, j, sX1, pstride, kXb - kSlotB);   // X1
+        cross_reduce<T>(part, ncol, 0, 1, sX0 + 63, pstride, kXa);                              // a
+        cross_reduce<T>(part, ncol, 0, 1, sX1 + 63, pstride, kXb);                              // b
         __syncthreads();
         // ---- column j-1 (every CTA, identical): H[:, j-1] = [c + X0; rho]
         const int k = j - 1, nc = j;
@@ -317,8 +360,8 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_dcgs2(Op A, FusedArgs<T> a) {
         // ---- one update pass: q_j -> V[:, j], candidate u' in place
         T e0d = T(0), e1d = T(0);
         dc_phase<T, kDcUpdate2>(a.V, a.ld, j, rb, re, u, z, a.V + (int64_t)j * a.ld, sX0, sY, rho, tau, a0, a1, e0d,
-                                e1d, (j + 1) & 1);
-        grid_sync(a.bar, nb);
+                                e1d, (j + 1) & 1, cmp);
+        MPK_DC_SYNC();
     }
 
     // ---------------- epilogue: d = R \ g, x_out = x0 + V_k d
@@ -326,6 +369,7 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_dcgs2(Op A, FusedArgs<T> a) {
     T *sd = sc;
     if (k > 0 && tid < 32) back_substitute<T>(a, k, ldr, sR, sg, sY, sd, lead, s_app);
     __syncthreads();
+    finish();
     if (k > 0 && s_app) return;   // TriangularBreakdownError: x_out untouched
     if (lead) {
         for (int i = tid; i < k; i += kFB) a.H.d[i] = sd[i];
@@ -338,7 +382,7 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_dcgs2(Op A, FusedArgs<T> a) {
     }
     T ext = T(0);
     reg_phase<T, kRegCorrect>(a.V, a.ld, k, rb, re, a.n, a.x0, a.x_out, sd, a0, ext);
-    (void)partC;
+#undef MPK_DC_SYNC
 }
 
 }  // namespace mpk

@@ -212,7 +212,8 @@ __device__ __forceinline__ void reg_write_partials(T (&acc)[RegCfg<T>::KP], int 
                 part[(int64_t)slot * kFMaxCtas + blockIdx.x] = s;
             } else {
                 const int64_t col = (int64_t)cm->rank * gridDim.x + blockIdx.x;
-                for (int q = 0; q < cm->nranks; ++q) cm->part[q][off + (int64_t)c * kXStride + col] = s;
+                const int slot = (c == kFExtra) ? xslot : c0 + c;
+                for (int q = 0; q < cm->nranks; ++q) cm->part[q][off + (int64_t)slot * kXStride + col] = s;
             }
         }
     }

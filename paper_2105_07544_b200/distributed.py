@@ -369,7 +369,7 @@ class _DistWs:
     def clear_changed(self):
         self.ws.clear_changed()
 
-    def cycle(self, prec, r0, rnorm2_off, x0, x_out, steps_cap, exit_tol, norm_scale, rule):
+    def cycle(self, prec, r0, rnorm2_off, x0, x_out, steps_cap, exit_tol, norm_scale, rule, orth="cgs2"):
         ws = self.ws
         d = ws.desc
         mat = self.s.op(prec)
@@ -394,7 +394,7 @@ class _DistWs:
         d.ws = ws.ws.ptr
         d.ctl = ws.ctl_ptr
         d.nranks = self.s.comm.size
-        d.flags = ws.flags
+        d.flags = ws.flags | (16 if orth == "dcgs2" else 0)
         d.comm = ctypes.pointer(self._comm_struct)
         _lib.check(D.lib().mpk_cycle_run(ctypes.byref(d), D.stream()))
 
@@ -471,7 +471,7 @@ def dist_gmres_restarted(sysm: LocalSystem, b, x0, cfg: SolverConfig, norm_basel
         if remaining <= 0 or restarts >= cfg.max_restarts:
             break
         cap = max(1, min(cfg.m, remaining))
-        ws.cycle(prec, r, OFF_RN2, x, x, cap, cfg.rtol, scale, cfg.breakdown_rule)
+        ws.cycle(prec, r, OFF_RN2, x, x, cap, cfg.rtol, scale, cfg.breakdown_rule, cfg.orthogonalization)
         ws.residual(prec, bd, x, r)
         out = ws.read(rn2_dtype=prec.dtype)
         state = CycleState(out.steps, out.implicit, scale, out.breakdown)
@@ -540,7 +540,8 @@ def dist_gmres_ir(sysm: LocalSystem, b, x0, cfg: IrConfig):
                 break
             continue
         cap = max(1, min(cfg.inner.m, remaining))
-        ws.cycle(low, r32, OFF_RN2_LOW, zeros32, u32, cap, floor, None, cfg.inner.breakdown_rule)
+        ws.cycle(low, r32, OFF_RN2_LOW, zeros32, u32, cap, floor, None, cfg.inner.breakdown_rule,
+                 cfg.inner.orthogonalization)
         ws.clear_changed()
         _lib.check(lib.mpk_ir_update(n, D.ptr(x), D.ptr(u32), ws.ws.at(OFF_CHANGED), D.stream()))
         ws.residual(prec, bd, x, r, r32)

@@ -129,3 +129,32 @@ def test_two_processes_share_the_gpu_through_ipc(cuda, tmp_path):
     assert r["fp64_iters"] == r["single_fp64_iters"] == 71
     assert abs(r["ir_iters"] - 150) <= 50
     assert r["x_maxdiff"] <= 1e-8
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_lagged_cgs2_row_partitioned(cuda, P):
+    """The one-reduction cycle across ranks (2 cross-rank barriers per step):
+    same counts as the single-GPU lagged cycle within a restart cycle."""
+    A = L("Laplace3D", 24)
+    A_low = mk.convert_matrix(A, P32)
+    b = np.ones(A.n)
+
+    def fn(comm):
+        sysm = dd.LocalSystem(comm, A, A_low)
+        try:
+            inner = mk.SolverConfig(m=50, rtol=1e-4, precision=P32, max_iters=20000, orthogonalization="dcgs2")
+            ir_rep = dd.dist_gmres_ir(sysm, b, np.zeros(A.n), mk.IrConfig(inner=inner, rtol=1e-10))
+            g64 = dd.dist_gmres_restarted(sysm, b, np.zeros(A.n),
+                                          mk.SolverConfig(m=50, rtol=1e-10, orthogonalization="dcgs2"))
+            return ir_rep.total_iters, ir_rep.converged, g64.total_iters, g64.converged, g64.final_explicit_relres
+        finally:
+            sysm.close()
+
+    res = dd.run_virtual_ranks(P, fn)
+    assert all(r == res[0] for r in res)
+    it_ir, c_ir, it64, c64, rel64 = res[0]
+    inner = mk.SolverConfig(m=50, rtol=1e-4, precision=P32, max_iters=20000, orthogonalization="dcgs2")
+    ref_ir = mk.gmres_ir(A, b, np.zeros(A.n), mk.IrConfig(inner=inner, rtol=1e-10))
+    ref64 = mk.gmres_restarted(A, None, b, np.zeros(A.n), mk.SolverConfig(m=50, rtol=1e-10, orthogonalization="dcgs2"))
+    assert c_ir and c64 and rel64 <= 1e-10
+    assert abs(it_ir - ref_ir.total_iters) <= 50 and abs(it64 - ref64.total_iters) <= 50
