@@ -657,18 +657,22 @@ int launch_fused_reg(const Op &op, const mpk_cycle_desc *d, int cap, double tf, 
     Ws ws = carve(d->ws);
     // layout of k_cycle_reg: small m keeps R (m+1 x m) in shared memory
     const bool big = m + 1 > kRegMaxCols;
-    auto kern = big ? k_cycle_reg<T, Op, true> : k_cycle_reg<T, Op, false>;
+    const bool multi = d->nranks > 1;
+    if (multi && big) return fail(MPK_EUNSUPPORTED, "row-partitioned cycles support m <= 51");
+    auto kern = multi ? k_cycle_reg<T, Op, false, true>
+                      : (big ? k_cycle_reg<T, Op, true, false> : k_cycle_reg<T, Op, false, false>);
     const size_t nslot = big ? (size_t)m + 2 : (size_t)kFSlots;
     const size_t smem = sizeof(T) * ((big ? 0 : (size_t)(m + 1) * m) + 2 * m + (m + 1) + 2 * nslot + kFW * kFSlots +
                                      (big ? nslot : 0) + kFW * kCsrWarpBuf);
-    static size_t attr_set[2] = {0, 0};
-    if (smem > attr_set[big]) {
+    static size_t attr_set[3] = {0, 0, 0};
+    const int vi = multi ? 2 : (big ? 1 : 0);
+    if (smem > attr_set[vi]) {
         cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (ea != cudaSuccess) {
             g_err = std::string("k_cycle_reg smem attribute: ") + cudaGetErrorString(ea);
             return MPK_ELAUNCH;
         }
-        attr_set[big] = smem;
+        attr_set[vi] = smem;
     }
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFB, smem);
@@ -722,17 +726,18 @@ int launch_dcgs2(const Op &op, const mpk_cycle_desc *d, int cap, double tf, doub
     const int m = d->m;
     T *w = (T *)d->work;
     Ws ws = carve(d->ws);
-    auto kern = k_cycle_dcgs2<T, Op>;
+    auto kern = d->nranks > 1 ? k_cycle_dcgs2<T, Op, true> : k_cycle_dcgs2<T, Op, false>;
     const size_t smem = sizeof(T) * (2 * (size_t)(m + 1) * m + 2 * m + (m + 1) + 5 * 64 + kFW * kFSlots +
                                      kFW * kCsrWarpBuf);
-    static size_t attr_set = 0;
-    if (smem > attr_set) {
+    static size_t attr_set[2] = {0, 0};
+    const int mi = d->nranks > 1 ? 1 : 0;
+    if (smem > attr_set[mi]) {
         cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (ea != cudaSuccess) {
             g_err = std::string("k_cycle_dcgs2 smem attribute: ") + cudaGetErrorString(ea);
             return MPK_ELAUNCH;
         }
-        attr_set = smem;
+        attr_set[mi] = smem;
     }
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFB, smem);

@@ -176,7 +176,7 @@ __device__ __noinline__ void dc_spmv(const Op &A, const T *x, T *y, int64_t rb, 
     }
 }
 
-template <typename T, class Op>
+template <typename T, class Op, bool MULTI>
 __global__ void __launch_bounds__(kFB, 1) k_cycle_dcgs2(Op A, FusedArgs<T> a) {
     using C = RegCfg<T>;
     extern __shared__ __align__(16) unsigned char dsm_dc[];
@@ -208,8 +208,8 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_dcgs2(Op A, FusedArgs<T> a) {
     // the candidate u lives in the rank's global-length x buffer (halo rows
     // mirrored P2P by the neighbours), barriers span all ranks.
     constexpr int kSlotB = 52, kXa = 104, kXb = 105;
-    const bool multi = a.cm.nranks > 1;
-    const CommArgs<T> *cmp = multi ? &a.cm : nullptr;
+    constexpr bool multi = MULTI;   // separate instantiations: the one-GPU kernel carries no comm code
+    const CommArgs<T> *cmp = MULTI ? &a.cm : nullptr;
     const int pstride = multi ? kXStride : kFMaxCtas;
     const unsigned ncol = multi ? nb * (unsigned)a.cm.nranks : nb;
     T *part = multi ? a.cm.part[a.cm.rank] : a.part;
@@ -299,10 +299,13 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_dcgs2(Op A, FusedArgs<T> a) {
         reg_write_partials<T>(a0, j, e0, sred, part, cmp, 0, 0, true, kXa);
         reg_write_partials<T>(a1, j, e1, sred, part, cmp, 0, kSlotB, true, kXb);
         MPK_DC_SYNC();
-        cross_reduce<T>(part, ncol, j, j, sX0, pstride, kXa);                                   // X0
-        cross_reduce<T>(part + (int64_t)kSlotB * pstride, ncol, j, j, sX1, pstride, kXb - kSlotB);   // X1
-        cross_reduce<T>(part, ncol, 0, 1, sX0 + 63, pstride, kXa);                              // a
-        cross_reduce<T>(part, ncol, 0, 1, sX1 + 63, pstride, kXb);                              // b
+        cross_reduce<T>(part, ncol, j, j + 1, sX0, pstride, kXa);                                   // X0, a
+        cross_reduce<T>(part + (int64_t)kSlotB * pstride, ncol, j, j + 1, sX1, pstride, kXb - kSlotB);   // X1, b
+        __syncthreads();
+        if (tid == 0) {
+            sX0[63] = sX0[j];
+            sX1[63] = sX1[j];
+        }
         __syncthreads();
         // ---- column j-1 (every CTA, identical): H[:, j-1] = [c + X0; rho]
         const int k = j - 1, nc = j;

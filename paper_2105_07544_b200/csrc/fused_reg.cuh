@@ -275,7 +275,7 @@ __device__ __noinline__ T phase_a_spmv(const Op &A, const XSlab<T> xs, T *w, int
     return an;
 }
 
-template <typename T, class Op, bool BIG>
+template <typename T, class Op, bool BIG, bool MULTI>
 __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
     using C = RegCfg<T>;
     extern __shared__ __align__(16) unsigned char dsm_reg[];
@@ -318,8 +318,8 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
     const int64_t rpc = ((a.n + nb - 1) / nb + 63) / 64 * 64;   // rows per CTA, 64-aligned
     const int64_t rb = (int64_t)blockIdx.x * rpc;
     const int64_t re = (rb + rpc < a.n) ? rb + rpc : a.n;
-    const bool multi = a.cm.nranks > 1;
-    const CommArgs<T> *cmp = multi ? &a.cm : nullptr;
+    constexpr bool multi = MULTI;   // separate instantiations: the one-GPU kernel carries no comm code
+    const CommArgs<T> *cmp = MULTI ? &a.cm : nullptr;
     // partials: single GPU -> local [slot][cta]; multi -> every rank's
     // [phase][slot][rank * nb + cta], reduced over nranks * nb columns
     const int64_t pblk = multi ? (int64_t)kFSlots * kXStride : (int64_t)nslot * kFMaxCtas;
