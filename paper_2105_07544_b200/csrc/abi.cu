@@ -767,6 +767,10 @@ int launch_dcgs2(const Op &op, const mpk_cycle_desc *d, int cap, double tf, doub
     fa.exit_tol = d->exit_tol;
     fa.norm_scale = d->norm_scale;
     fa.u = u;
+    fa.diag = nullptr;
+    fa.z = w + 3 * d->ld;
+    if (d->M && d->M->kind == MPK_PC_JACOBI && d->M->block == 1 && d->M->dtype == d->dtype)
+        fa.diag = (const T *)d->M->lu;
     if (int rc = fill_comm<T>(fa, d, grid)) return rc;
     Op opc = op;
     void *args[] = {(void *)&opc, (void *)&fa};
@@ -810,7 +814,7 @@ template <typename T> int run_cycle(const mpk_cycle_desc *d, cudaStream_t s) {
     // register kernel applies it inside its SpMV input and correction
     const bool diag1 = precond && d->M->kind == MPK_PC_JACOBI && d->M->block == 1 && d->M->n == n &&
                        d->M->dtype == d->dtype;
-    if ((d->flags & 16) && !precond && m + 1 <= kRegMaxCols &&
+    if ((d->flags & 16) && (!precond || (diag1 && d->nranks <= 1)) && m + 1 <= kRegMaxCols &&
         (uintptr_t)d->x_out % 16 == 0 &&
         (uintptr_t)d->V % 16 == 0 && (uintptr_t)d->work % 16 == 0 && (uintptr_t)d->r0 % 16 == 0) {
         return with_op<T>(d->A, [&](auto op) -> int { return launch_dcgs2<T, decltype(op)>(op, d, cap, tf, u, s); });

@@ -2,8 +2,8 @@
 // mathematically the reference's CGS2 Arnoldi (kernels.py:98-126), reordered
 // so each step needs ONE global reduction and TWO passes over the basis
 // (the reference's form needs 4 passes; k_cycle_reg needs 3 and 3 grid
-// barriers).  Opt-in (SolverConfig.orthogonalization = "dcgs2"); identity
-// preconditioner, m <= 51, one GPU.
+// barriers).  Opt-in (SolverConfig.orthogonalization = "dcgs2"); identity or
+// diagonal (block Jacobi k = 1, one GPU) right preconditioner, m <= 51.
 //
 // State entering step j (1..m): Q_j = [q_0..q_{j-1}] (final), u = w_{j-1} -
 // Q_j c (w_{j-1} = A q_{j-1} after its first CGS pass c, neither
@@ -152,10 +152,23 @@ __device__ __forceinline__ void dc_phase(const T *V, int64_t ld, int nc, int64_t
     else dc_phase_u<T, MODE, 1>(V, ld, nc, rb, re, u, z, qout, X0, Y, rho, tau, a0, a1, e0, e1, rev, cm);
 }
 
+// ... scaled by a diagonal right preconditioner: x = M u = u / a_ii
+// (block Jacobi k = 1, preconditioners.py:133-139: one IEEE division)
+template <typename T> struct XCgDiag {
+    const T *p;
+    const T *diag;
+    __device__ __forceinline__ T operator()(int64_t c) const { return RN<T>::div(__ldcg(p + c), __ldg(diag + c)); }
+    __device__ __forceinline__ Pack<T> vec(int64_t c) const {
+        Pack<T> q = ldcg16(p + c);
+#pragma unroll
+        for (int e = 0; e < (int)(16 / sizeof(T)); ++e) q.v[e] = RN<T>::div(q.v[e], __ldg(diag + c + e));
+        return q;
+    }
+};
+
 // SpMV of the candidate: y = A x over the CTA's rows, x read through L2.
-template <typename T, class Op>
-__device__ __noinline__ void dc_spmv(const Op &A, const T *x, T *y, int64_t rb, int64_t re, T *sstage) {
-    const XCg<T> xs{x};
+template <typename T, class Op, class X>
+__device__ __noinline__ void dc_spmv_x(const Op &A, const X xs, T *y, int64_t rb, int64_t re, T *sstage) {
     if constexpr (!Op::kStencil) {
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         T *sb = sstage + warp * kCsrWarpBuf;
@@ -174,6 +187,13 @@ __device__ __noinline__ void dc_spmv(const Op &A, const T *x, T *y, int64_t rb, 
     } else {
         for (int64_t r = rb + threadIdx.x; r < re; r += kFB) y[r] = A.row(r, xs);
     }
+}
+
+template <typename T, class Op>
+__device__ __forceinline__ void dc_spmv(const Op &A, const T *x, const T *diag, T *y, int64_t rb, int64_t re,
+                                        T *sstage) {
+    if (diag) dc_spmv_x<T>(A, XCgDiag<T>{x, diag}, y, rb, re, sstage);
+    else dc_spmv_x<T>(A, XCg<T>{x}, y, rb, re, sstage);
 }
 
 template <typename T, class Op, bool MULTI>
@@ -272,9 +292,13 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_dcgs2(Op A, FusedArgs<T> a) {
             src = u;
             MPK_DC_SYNC();
         }
-        for (int64_t r = rb + tid; r < re; r += kFB) q0[r] = RN<T>::div(__ldcg(src + r), gm);
+        for (int64_t r = rb + tid; r < re; r += kFB) {
+            const T v = RN<T>::div(__ldcg(src + r), gm);
+            q0[r] = v;
+            if (a.diag) a.z[r] = RN<T>::div(v, __ldg(a.diag + r));   // M q_0 on the own rows
+        }
         __syncthreads();
-        phase_a_spmv<T>(A, XSlab<T>{src, q0, gm, rb, re, nullptr, nullptr}, z, rb, re, sstage);
+        phase_a_spmv<T>(A, XSlab<T>{src, q0, gm, rb, re, a.diag, a.z}, z, rb, re, sstage);
         __syncthreads();
 #pragma unroll
         for (int i = 0; i < C::KP; ++i) a0[i] = T(0);
@@ -289,7 +313,7 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_dcgs2(Op A, FusedArgs<T> a) {
     }
     // ---- steps j = 1..cap: finalise column j-1, build q_j and the next candidate
     for (int j = 1; j <= a.cap && !s_done; ++j) {
-        dc_spmv<T>(A, u, z, rb, re, sstage);   // z = A u
+        dc_spmv<T>(A, u, a.diag, z, rb, re, sstage);   // z = A M u
         __syncthreads();
         T e0 = T(0), e1 = T(0);
 #pragma unroll
@@ -384,7 +408,7 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_dcgs2(Op A, FusedArgs<T> a) {
         return;
     }
     T ext = T(0);
-    reg_phase<T, kRegCorrect>(a.V, a.ld, k, rb, re, a.n, a.x0, a.x_out, sd, a0, ext);
+    reg_phase<T, kRegCorrect>(a.V, a.ld, k, rb, re, a.n, a.x0, a.x_out, sd, a0, ext, nullptr, a.diag);   // x0 + M V_k d
 #undef MPK_DC_SYNC
 }
 

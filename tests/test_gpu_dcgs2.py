@@ -65,3 +65,21 @@ def test_lucky_breakdown_detected(cuda):
     _, st = mk.gmres_cycle(A, None, np.ones(16), np.zeros(16), cfg)
     _, st2 = mk.gmres_cycle(A, None, np.ones(16), np.zeros(16), mk.SolverConfig(m=10, rtol=1e-300))
     assert st.breakdown and st2.breakdown and st.steps == st2.steps
+
+
+def test_jacobi1_lagged_matches_cgs2(cuda):
+    """Block Jacobi k=1 inside the lagged cycle (SpMV input M u, correction
+    x0 + M V d): same convergence as the CGS2 kernel."""
+    A = mk.synthetic_irregular(12000, band=300, signs="negative", dominance=1.01, shift=1e-3)
+    b = np.ones(A.n)
+    J = mk.build_block_jacobi(A, 1)
+    r1 = mk.gmres_restarted(A, J, b, np.zeros(A.n), mk.SolverConfig(m=50, rtol=1e-10, max_iters=5000))
+    r2 = mk.gmres_restarted(A, J, b, np.zeros(A.n), mk.SolverConfig(m=50, rtol=1e-10, max_iters=5000,
+                                                                    orthogonalization="dcgs2"))
+    assert r1.converged and r2.converged and abs(r1.total_iters - r2.total_iters) <= 50
+    assert np.abs(r1.x - r2.x).max() <= 1e-7 * np.abs(r1.x).max()
+    Al = mk.convert_matrix(A, P.binary32)
+    J32 = mk.build_block_jacobi(Al, 1)
+    inner = mk.SolverConfig(m=50, rtol=1e-4, precision=P.binary32, max_iters=5000, orthogonalization="dcgs2")
+    ir = mk.gmres_ir(A, b, np.zeros(A.n), mk.IrConfig(inner=inner, rtol=1e-10), M=J32, A_low=Al)
+    assert ir.converged and ir.final_explicit_relres <= 1e-10
