@@ -172,8 +172,9 @@ __device__ __noinline__ void dc_spmv_x(const Op &A, const X xs, T *y, int64_t rb
     if constexpr (!Op::kStencil) {
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         T *sb = sstage + warp * kCsrWarpBuf;
+        const bool wide = sizeof(T) == 4 && A.rp[A.n] > 16 * (int64_t)A.n;   // long rows: 16 entries per lane
         for (int64_t r0 = rb + (int64_t)warp * 32; r0 < re; r0 += (int64_t)kFW * 32) {
-            const T yr = A.template warp_rows<8>(r0, re, xs, sb);
+            const T yr = wide ? A.template warp_rows<16>(r0, re, xs, sb) : A.template warp_rows<8>(r0, re, xs, sb);
             if (r0 + lane < re) y[r0 + lane] = yr;
         }
     } else if (A.group_ok()) {
