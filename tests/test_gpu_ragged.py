@@ -15,11 +15,11 @@ P = mk.Precision
 SIZES = (1, 2, 3, 5, 7, 63, 65, 130, 1001)
 
 
-def _system(n, seed=7):
+def _system(n, seed=7, diag_shift=None):
     rng = np.random.default_rng(seed + n)
     from conftest import random_csr
 
-    return random_csr(mk, rng, n, density=min(1.0, 8.0 / n + 0.02))
+    return random_csr(mk, rng, n, density=min(1.0, 8.0 / n + 0.02), diag_shift=diag_shift)
 
 
 @pytest.mark.parametrize("orth", ["cgs2", "dcgs2"])
@@ -60,3 +60,25 @@ def test_restarted_and_ir_ragged(cuda, n, orth):
     ir = mk.gmres_ir(A, b, np.zeros(n), mk.IrConfig(inner=inner, rtol=1e-12))
     assert ir.converged and ir.final_explicit_relres <= 1e-12
     assert np.abs(ir.x - want).max() <= 1e-10 * np.abs(want).max()
+
+
+@pytest.mark.parametrize("orth", ["cgs2", "dcgs2"])
+@pytest.mark.parametrize("n", (63, 65, 130, 1001))
+def test_one_cycle_fp32_vs_oracle(cuda, n, orth):
+    """fp32 cycle (the GMRES-IR inner solver) on odd sizes: the oracle in
+    float32 (same roundings, sequential sums) is the checker; the device's
+    fixed-order tree sums differ in the last bits only."""
+    from oracle import mpk_oracle as O
+
+    A64, _ = _system(n, diag_shift=3.0)   # slow convergence: all 20 steps above 1e-5
+    A = mk.convert_matrix(A64, P.binary32)
+    b = np.random.default_rng(n).standard_normal(n).astype(np.float32)
+    cfg = mk.SolverConfig(m=20, rtol=1e-300, precision=P.binary32, orthogonalization=orth)
+    x, st = mk.gmres_cycle(A, None, b, np.zeros(n, np.float32), cfg)
+    xo, so = O.one_cycle((A.row_ptr, A.col_idx, A.values), None, b, np.zeros(n, np.float32), 20, 1e-300)
+    h, ho = np.array(st.implicit_relres), np.array(so.implicit)
+    k = min(len(h), len(ho))
+    keep = ho[:k] > 1e-5
+    assert keep.sum() >= 8
+    assert np.all(np.abs(h[:k] - ho[:k])[keep] <= 2e-3 * ho[:k][keep])
+    assert np.abs(x.astype(np.float64) - xo).max() <= 1e-3 * np.abs(xo).max()
