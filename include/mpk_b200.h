@@ -187,6 +187,21 @@ int mpk_dev_free(void *ptr);
 int mpk_ipc_get(const void *ptr, void *handle64);
 int mpk_ipc_open(const void *handle64, void **ptr);
 int mpk_ipc_close(void *ptr);
+/* 1 when device `dev` can map `peer`'s memory (cudaDeviceCanAccessPeer; 1
+ * for dev == peer), 0 when it cannot; the communicator refuses to build on 0 */
+int mpk_can_access_peer(int32_t dev, int32_t peer);
+/* Per-restart collectives of the row-partitioned solve (gmres.py:290-291,
+ * multiprecision.py:216-217 across ranks), device-side over the same peer
+ * buffers and arrival counters as the cycle kernel; `dtype` names the
+ * communicator's precision set.
+ * push_rows: x (n local rows) -> own xg at row0, mirror rows -> the peers'
+ *   xg, then a cross-rank barrier; the residual then reads xg's halo.
+ * reduce_ctl: the 32-byte slot {r.r (dtype rn2_dtype), r_low.r_low (f32),
+ *   moved (i32), timeout (i32, out), b.b (dtype bn2_dtype)} summed over the
+ *   ranks in rank order, in place. */
+int mpk_comm_push_rows(const mpk_comm *c, int32_t dtype, int64_t n, const void *x, void *stream);
+int mpk_comm_reduce_ctl(const mpk_comm *c, int32_t dtype, void *slot32, int32_t rn2_dtype, int32_t bn2_dtype,
+                        void *stream);
 
 /* ------------------------------------------------------------------ */
 /* restarted GMRES cycle (gmres.py:134-205)                            */
@@ -290,6 +305,10 @@ int mpk_rcm_host(int64_t n, const int64_t *indptr, const int64_t *indices, int64
 int mpk_prof_reset(void);
 /* number of kernels this library has enqueued so far (monotonic) */
 int64_t mpk_launch_count(void);
+/* kernel family the calling thread's last mpk_cycle_run launched
+ * ("k_cycle_reg", "k_cycle_reg/big", "k_cycle_reg/multi", "k_cycle_dcgs2",
+ * "k_cycle_dcgs2/multi", "k_cycle_fused", "multi-kernel"); diagnostics/tests */
+const char *mpk_last_cycle_kernel(void);
 /* totals[c] = summed milliseconds, counts[c] = launches, bytes[c] = algorithmic bytes */
 int mpk_prof_read(double *ms, int64_t *counts, double *bytes, int32_t nclasses);
 /* per-CTA clock64 totals of the persistent cycle's sections (16 slots per

@@ -29,6 +29,7 @@ EXPORTS = (
     "mpk_precond_apply", "mpk_prof_reset", "mpk_prof_read", "mpk_lsq_init", "mpk_lsq_update",
     "mpk_lsq_solve", "mpk_vdiv", "mpk_launch_count", "mpk_fused_prof_read", "mpk_comm_part_bytes",
     "mpk_dev_alloc", "mpk_dev_free", "mpk_ipc_get", "mpk_ipc_open", "mpk_ipc_close", "mpk_rcm_host",
+    "mpk_last_cycle_kernel", "mpk_can_access_peer", "mpk_comm_push_rows", "mpk_comm_reduce_ctl",
 )
 MAX_RANKS = 8
 
@@ -117,6 +118,10 @@ _SIGS = {
                              ctypes.POINTER(ctypes.c_double), _I32]),
 }
 _SIGS["mpk_launch_count"] = (_I64, [])
+_SIGS["mpk_last_cycle_kernel"] = (ctypes.c_char_p, [])
+_SIGS["mpk_can_access_peer"] = (_I32, [_I32, _I32])
+_SIGS["mpk_comm_push_rows"] = (_I32, [ctypes.c_void_p, _I32, _I64, _P, _P])
+_SIGS["mpk_comm_reduce_ctl"] = (_I32, [ctypes.c_void_p, _I32, _P, _I32, _I32, _P])
 _SIGS["mpk_fused_prof_read"] = (_I32, [ctypes.POINTER(ctypes.c_uint64), _I32])
 _SIGS["mpk_comm_part_bytes"] = (_I64, [_I32])
 _SIGS["mpk_dev_alloc"] = (_I32, [_I64, ctypes.POINTER(ctypes.c_void_p)])
@@ -150,6 +155,11 @@ def load(require_device: bool = True):
         if not torch.cuda.is_available():
             raise NativeUnavailable("no CUDA device: the B200 path has no CPU fallback")
     return _LIB
+
+
+def last_cycle_kernel() -> str:
+    """Kernel family of this thread's last mpk_cycle_run (tests prove dispatch with it)."""
+    return load(require_device=False).mpk_last_cycle_kernel().decode()
 
 
 def check(rc: int):

@@ -17,6 +17,7 @@
 #include <utility>
 #include <vector>
 
+#include "comm.cuh"
 #include "fused_dcgs2.cuh"
 
 using namespace mpk;
@@ -25,6 +26,7 @@ namespace {
 
 thread_local std::string g_err;
 unsigned long long g_launches = 0;   // kernels enqueued by this library
+thread_local const char *g_last_cycle = "";   // kernel family of the last mpk_cycle_run
 
 int fail(int code, const char *msg) {
     g_err = msg;
@@ -587,7 +589,32 @@ int launch_fused(const Op &op, const mpk_cycle_desc *d, int cap, double tf, doub
         g_err = std::string("k_cycle_fused: ") + cudaGetErrorString(e);
         return MPK_ELAUNCH;
     }
+    g_last_cycle = "k_cycle_fused";
     return check_launch("k_cycle_fused");
+}
+
+int64_t comm_part_core(int32_t dtype) { return 3LL * kFSlots * kXStride * (dtype == MPK_F64 ? 8 : 4); }
+
+// the per-restart collectives' view of a communicator (comm.cuh); `dtype` =
+// the precision set the buffers belong to
+int comm_view(const mpk_comm *c, int32_t dtype, CommView &v) {
+    memset(&v, 0, sizeof(v));
+    if (!c || c->nranks < 1 || c->nranks > kMaxRanks || c->rank < 0 || c->rank >= c->nranks || !c->epoch)
+        return fail(MPK_EARG, "inconsistent mpk_comm");
+    v.rank = c->rank;
+    v.nranks = c->nranks;
+    v.row0 = c->row0;
+    v.epoch = (unsigned long long *)c->epoch;
+    const int64_t core = comm_part_core(dtype);
+    for (int q = 0; q < c->nranks; ++q) {
+        if (!c->part[q] || !c->xbar[q] || !c->xg[q]) return fail(MPK_EARG, "null peer pointer");
+        v.xg[q] = (char *)c->xg[q];
+        v.xbar[q] = (unsigned long long *)c->xbar[q];
+        v.scal[q] = (char *)c->part[q] + core;
+        v.mir_lo[q] = c->mir_lo[q];
+        v.mir_hi[q] = c->mir_hi[q];
+    }
+    return MPK_OK;
 }
 
 // Persistent cycle variant: "reg" (16-byte register streaming, default) or
@@ -716,6 +743,7 @@ int launch_fused_reg(const Op &op, const mpk_cycle_desc *d, int cap, double tf, 
         g_err = std::string("k_cycle_reg: ") + cudaGetErrorString(e);
         return MPK_ELAUNCH;
     }
+    g_last_cycle = multi ? "k_cycle_reg/multi" : (big ? "k_cycle_reg/big" : "k_cycle_reg");
     return check_launch("k_cycle_reg");
 }
 
@@ -780,6 +808,7 @@ int launch_dcgs2(const Op &op, const mpk_cycle_desc *d, int cap, double tf, doub
         g_err = std::string("k_cycle_dcgs2: ") + cudaGetErrorString(e);
         return MPK_ELAUNCH;
     }
+    g_last_cycle = d->nranks > 1 ? "k_cycle_dcgs2/multi" : "k_cycle_dcgs2";
     return check_launch("k_cycle_dcgs2");
 }
 
@@ -806,6 +835,8 @@ template <typename T> int run_cycle(const mpk_cycle_desc *d, cudaStream_t s) {
             (uintptr_t)d->work % 16 || (uintptr_t)d->r0 % 16)
             return fail(MPK_EUNSUPPORTED, "row-partitioned cycle: identity preconditioner, m <= 51, "
                                           "16-byte aligned buffers");
+        if (d->flags & 16)   // lagged one-reduction CGS2, row-partitioned instantiation
+            return with_op<T>(d->A, [&](auto op) -> int { return launch_dcgs2<T, decltype(op)>(op, d, cap, tf, u, s); });
         return with_op<T>(d->A, [&](auto op) -> int {
             return launch_fused_reg<T, decltype(op)>(op, d, cap, tf, u, s);
         });
@@ -848,6 +879,7 @@ template <typename T> int run_cycle(const mpk_cycle_desc *d, cudaStream_t s) {
         });
     }
 
+    g_last_cycle = "multi-kernel";
     k_cycle_begin<T><<<1, 32, 0, s>>>((const T *)d->rnorm2, sums, H, ctl, d->norm_scale);
     if ((rc = check_launch("k_cycle_begin"))) return rc;
 
@@ -1125,6 +1157,11 @@ int mpk_residual(const mpk_matrix *A, const void *b, const void *x, void *r, voi
 int mpk_ir_update(int64_t n, double *x, const float *u, int32_t *changed, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     int g = grid_for(k_ir_update, 0, n);
+    // the "x moved" flag is this refinement's: cleared stream-ordered here
+    if (changed) {
+        cudaError_t e = cudaMemsetAsync(changed, 0, sizeof(int32_t), s);
+        if (e != cudaSuccess) return fail(MPK_ELAUNCH, cudaGetErrorString(e));
+    }
     k_ir_update<<<g, kBlock, 0, s>>>(n, x, u, changed);
     return check_launch("k_ir_update");
 }
@@ -1174,6 +1211,7 @@ int mpk_lsq_solve(int32_t dtype, int32_t m, int32_t k, void *hess, mpk_cycle_ctl
 }
 
 int64_t mpk_launch_count(void) { return (int64_t)g_launches; }
+const char *mpk_last_cycle_kernel(void) { return g_last_cycle; }
 
 int mpk_prof_reset(void) {
     prof_drain(true);
@@ -1186,7 +1224,39 @@ int mpk_prof_reset(void) {
 }
 
 int64_t mpk_comm_part_bytes(int32_t dtype) {
-    return 3LL * kFSlots * kXStride * (dtype == MPK_F64 ? 8 : 4);
+    // cycle partials, then the per-restart scalar slot table (comm.cuh)
+    return comm_part_core(dtype) + (int64_t)kMaxRanks * kCommScalBytes;
+}
+
+int mpk_can_access_peer(int32_t dev, int32_t peer) {
+    if (dev == peer) return 1;
+    int ok = 0;
+    cudaError_t e = cudaDeviceCanAccessPeer(&ok, dev, peer);
+    if (e != cudaSuccess) return fail(MPK_ELAUNCH, cudaGetErrorString(e));
+    return ok ? 1 : 0;
+}
+
+int mpk_comm_push_rows(const mpk_comm *c, int32_t dtype, int64_t n, const void *x, void *stream) {
+    CommView v;
+    if (int rc = comm_view(c, dtype, v)) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    int64_t g = (n + 255) / 256;
+    const int64_t cap = (int64_t)sm_count_cached() * 4;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    if (dtype == MPK_F64) k_comm_push<double><<<(int)g, 256, 0, s>>>(v, n, (const double *)x);
+    else k_comm_push<float><<<(int)g, 256, 0, s>>>(v, n, (const float *)x);
+    return check_launch("k_comm_push");
+}
+
+int mpk_comm_reduce_ctl(const mpk_comm *c, int32_t dtype, void *slot32, int32_t rn2_dtype, int32_t bn2_dtype,
+                        void *stream) {
+    CommView v;
+    if (int rc = comm_view(c, dtype, v)) return rc;
+    if ((uintptr_t)slot32 % 16) return fail(MPK_EARG, "scalar slot must be 16-byte aligned");
+    k_comm_reduce<<<1, 32, 0, (cudaStream_t)stream>>>(v, (char *)slot32, rn2_dtype == MPK_F64,
+                                                       bn2_dtype == MPK_F64);
+    return check_launch("k_comm_reduce");
 }
 
 int mpk_dev_alloc(int64_t bytes, void **ptr) {

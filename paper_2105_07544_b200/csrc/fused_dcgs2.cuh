@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_dcgs2(Op A, FusedArgs<T> a) {
     T *sred = scol + 64;                       // kFW * kFSlots
     T *sstage = sred + kFW * kFSlots;          // kFW * kCsrWarpBuf
     __shared__ T s_gamma, s_rho, s_tau, s_beta;
-    __shared__ int s_done, s_steps, s_break, s_app;
+    __shared__ int s_done, s_steps, s_break, s_app, s_trunc;
     __shared__ double s_scale;
 
     const int tid = threadIdx.x;
@@ -348,8 +348,17 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_dcgs2(Op A, FusedArgs<T> a) {
             // (numerically) inside span(Q_j): treated as the reference's
             // lucky breakdown (beta = 0, kernels.py:122-126), which ends the
             // cycle with column j-1 included
+            // Below the guard the step is NOT declared a lucky breakdown
+            // (that would zero the implicit residual and can raise a false
+            // loss of accuracy): rho is clamped to the guard and the cycle
+            // ends after this column as if it had reached its cap, so the
+            // restart recomputes the explicit residual from scratch.
             const T eta = sizeof(T) == 4 ? T(1e-3) : T(1e-11);
-            if (!(rho2 > eta * av)) rho2 = T(0);
+            s_trunc = 0;
+            if (!(rho2 > eta * av)) {
+                rho2 = eta * av;
+                s_trunc = 1;
+            }
             const T rho = RN<T>::sqrt_(rho2);
             s_rho = rho;
             const T t = RN<T>::div(RN<T>::sub(bv, x0x1), rho);
@@ -373,7 +382,12 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_dcgs2(Op A, FusedArgs<T> a) {
             givens_step<T>(a, k, nc, ldr, scol, sY[62], sY[63], s_scale, lead, scs, ssn, sg, s_beta, s_steps,
                            s_done, s_break);
         __syncthreads();
+        if (tid == 0 && s_trunc && !s_done) {
+            s_done = 1;
+            if (lead) a.ctl->done = 1;
+        }
         for (int i = tid; i <= nc; i += kFB) sR[(int64_t)k * ldr + i] = scol[i];
+        __syncthreads();   // column k of R (all warps) before back_substitute (warp 0) or the next step
         if (s_done) break;
         // ---- next candidate: c' = ([X1; t] - H[:j+1, :j] X0)/rho ; Y = X1 - X0 tau
         const T rho = s_rho, tau = s_tau;

@@ -533,6 +533,10 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
         if (big)   // every CTA keeps its own (identical) copy of R in global memory
             for (int i = tid; i <= nc; i += kFB) sR[(int64_t)k * ldr + i] = col[i];
     }
+    // R's last column was stored by several warps (global memory when big):
+    // visible to back_substitute's warp 0 regardless of profiling
+    __threadfence_block();
+    __syncthreads();
 
     MPK_MARK(11);
     // ---------------- epilogue: d = R \ g, x_out = x0 + V_k d

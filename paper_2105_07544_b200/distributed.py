@@ -17,8 +17,13 @@ a contiguous row-block partition of the system across the GPUs of a box:
   partials in one fixed order, so every rank holds bit-identical Arnoldi
   coefficients and runs the same Givens update (no NCCL call inside the
   cycle, no host round trip);
-* once per restart / refinement the host allgathers x for the explicit
-  residual and sums three scalars across ranks (``Comm``).
+* once per restart / refinement two small device kernels do the rest over
+  the same peer memory and arrival counters: ``mpk_comm_push_rows`` stores
+  the rank's x rows into its global-length buffer and the mirror rows into
+  the neighbours' (the explicit residual reads its halo there), and
+  ``mpk_comm_reduce_ctl`` sums r.r, r_low.r_low, b.b and the "x moved" flag
+  over the ranks in rank order; the host then reads one control block, as
+  on one GPU (no pickling, no NCCL, no full-x allgather).
 
 Two communicators implement ``Comm``: :class:`TorchComm` (one process per
 GPU under torchrun, NCCL/gloo for the per-restart collectives and for the
@@ -37,7 +42,9 @@ import numpy as np
 
 from . import _lib
 from . import device as D
-from .engine import CTL_BYTES, OFF_BN2, OFF_CHANGED, OFF_RN2, OFF_RN2_LOW, CycleWorkspace, Readout, sqrt_in
+from .engine import OFF_BN2, OFF_CHANGED, OFF_RN2, OFF_RN2_LOW, CycleWorkspace, Readout, sqrt_in
+
+OFF_TIMEOUT = OFF_RN2 + 20   # int32 set by mpk_comm_reduce_ctl when a cross-rank barrier timed out
 from .errors import DimensionMismatchError, ZeroRightHandSideError
 from .gmres import ConvergenceReport, CycleState, HistoryEntry, SolverConfig, detect_loss_of_accuracy
 from .multiprecision import IrConfig
@@ -173,6 +180,21 @@ class TorchComm:
         self.rank, self.size = dist.get_rank(), dist.get_world_size()
         self.ctas = 0
         self.ipc = True
+        if D.torch().cuda.is_available():   # host-only (gloo) tests have no device to map
+            self.check_peers()
+
+    def check_peers(self):
+        """Every rank must be able to map every other rank's memory (P2P over
+        NVLink); refuse loudly otherwise instead of faulting in the kernel."""
+        t = D.torch()
+        dev = t.cuda.current_device()
+        devs = self.exchange(dev)
+        lib = D.lib()
+        for q, pd in enumerate(devs):
+            ok = int(lib.mpk_can_access_peer(dev, pd))
+            if ok != 1:
+                raise RuntimeError("rank %d (cuda:%d) cannot access rank %d's device cuda:%d peer-to-peer"
+                                   % (self.rank, dev, q, pd))
 
     def exchange(self, obj) -> list:
         out = [None] * self.size
@@ -277,9 +299,6 @@ class LocalSystem:
                 self.ops[prec] = self._local_op(M)
         self._peers = {}
         self._ws = {}
-        t = D.torch()
-        self.x_glob = t.zeros(D.ld_for(self.n_global) + ALIGN, dtype=t.float64, device=D.device())
-        self.ctl = t.zeros(CTL_BYTES + 256, dtype=t.uint8, device=D.device())
 
     def _local_op(self, M: CsrMatrix):
         d = _lib.MpkMatrix()
@@ -351,23 +370,27 @@ class _DistWs:
         self.ws = sysm.workspace(m, prec)
         self.prec = prec
         self._comm_struct = sysm.comm_struct(prec)
+        self._push_prec = prec
 
     def residual(self, prec, b, x, r, r_low=None):
-        """r = b - A x on the rank's rows; x's halo comes from an allgather."""
+        """r = b - A x on the rank's rows.  x (precision `prec`) goes into the
+        rank's global-length buffer of that precision set and its mirror rows
+        into the neighbours' (mpk_comm_push_rows, P2P + cross-rank barrier);
+        the residual kernel reads its halo there."""
         s = self.s
-        s.comm.allgather_rows(x, s.x_glob, s.starts)
-        xv = s.x_glob[s.r0:]
+        lib = D.lib()
+        cs = s.comm_struct(prec)
+        _lib.check(lib.mpk_comm_push_rows(ctypes.addressof(cs), prec.code, s.n, D.ptr(x), D.stream()))
+        xv = s.peers(prec).own["xg"] + s.r0 * prec.dtype.itemsize
         d = s.op(prec)
-        _lib.check(D.lib().mpk_residual(ctypes.byref(d), D.ptr(b), D.ptr(xv), D.ptr(r),
-                                        self.ws.at(OFF_RN2), D.ptr(r_low) if r_low is not None else None,
-                                        self.ws.at(OFF_RN2_LOW) if r_low is not None else None,
-                                        self.ws.ws.ptr, D.stream()))
+        _lib.check(lib.mpk_residual(ctypes.byref(d), D.ptr(b), xv, D.ptr(r),
+                                    self.ws.at(OFF_RN2), D.ptr(r_low) if r_low is not None else None,
+                                    self.ws.at(OFF_RN2_LOW) if r_low is not None else None,
+                                    self.ws.ws.ptr, D.stream()))
+        self._push_prec = prec
 
     def bnorm2(self, b, prec):
         self.ws.bnorm2(b, prec)
-
-    def clear_changed(self):
-        self.ws.clear_changed()
 
     def cycle(self, prec, r0, rnorm2_off, x0, x_out, steps_cap, exit_tol, norm_scale, rule, orth="cgs2"):
         ws = self.ws
@@ -399,24 +422,23 @@ class _DistWs:
         _lib.check(D.lib().mpk_cycle_run(ctypes.byref(d), D.stream()))
 
     def read(self, rn2_dtype=np.float64, with_cycle=True, bn2_dtype=None) -> Readout:
-        """Local control block + the rank sums of r.r, r_low.r_low, b.b and
-        the 'moved' flag; the global sums are written back to the device
-        slots the next cycle reads."""
+        """Sum r.r, r_low.r_low, b.b and the 'moved' flag over the ranks on
+        the device (mpk_comm_reduce_ctl, rank order, in place in the slots the
+        next cycle reads), then the one control-block read of a restart."""
+        prec = self._push_prec
+        rt = np.dtype(rn2_dtype)
+        bt = np.dtype(bn2_dtype or rn2_dtype)
+        code = lambda dt: _lib.F64 if dt == np.float64 else _lib.F32  # noqa: E731
+        cs = self.s.comm_struct(prec)
+        _lib.check(D.lib().mpk_comm_reduce_ctl(ctypes.addressof(cs), prec.code, self.ws.at(OFF_RN2),
+                                               code(rt), code(bt), D.stream()))
         out = self.ws.read(rn2_dtype=rn2_dtype, with_cycle=with_cycle)
         raw = self.ws.host.numpy()
-        if with_cycle and int(np.frombuffer(raw, dtype=np.int32, count=6, offset=0)[5]):
-            raise RuntimeError("row-partitioned cycle: a rank missed the cross-GPU barrier (timeout)")
-        rt = np.dtype(rn2_dtype).type
-        bt = np.dtype(bn2_dtype or rn2_dtype).type
-        bn2 = np.frombuffer(raw, dtype=bt, count=1, offset=OFF_BN2)[0]
-        loc = [rt(out.rn2), np.float32(out.rn2_low), bt(bn2), int(out.changed)]
-        g = self.s.comm.allreduce_host(loc)
-        host = np.zeros(32, dtype=np.uint8)
-        host[0:np.dtype(rt).itemsize] = np.frombuffer(rt(g[0]).tobytes(), dtype=np.uint8)
-        host[8:12] = np.frombuffer(np.float32(g[1]).tobytes(), dtype=np.uint8)
-        self.ws.ctlbuf[OFF_RN2:OFF_RN2 + 16].copy_(D.torch().from_numpy(host[:16]))
-        self._bn2 = float(g[2])
-        return dataclasses.replace(out, rn2=float(g[0]), rn2_low=float(g[1]), changed=bool(g[3]))
+        if int(np.frombuffer(raw, dtype=np.int32, count=1, offset=OFF_TIMEOUT)[0]) or \
+                (with_cycle and int(np.frombuffer(raw, dtype=np.int32, count=6, offset=0)[5])):
+            raise RuntimeError("row-partitioned solve: a rank missed the cross-GPU barrier (timeout)")
+        self._bn2 = float(np.frombuffer(raw, dtype=bt, count=1, offset=OFF_BN2)[0])
+        return out
 
     def bn2(self) -> float:
         return self._bn2
@@ -542,7 +564,6 @@ def dist_gmres_ir(sysm: LocalSystem, b, x0, cfg: IrConfig):
         cap = max(1, min(cfg.inner.m, remaining))
         ws.cycle(low, r32, OFF_RN2_LOW, zeros32, u32, cap, floor, None, cfg.inner.breakdown_rule,
                  cfg.inner.orthogonalization)
-        ws.clear_changed()
         _lib.check(lib.mpk_ir_update(n, D.ptr(x), D.ptr(u32), ws.ws.at(OFF_CHANGED), D.stream()))
         ws.residual(prec, bd, x, r, r32)
         out = ws.read()

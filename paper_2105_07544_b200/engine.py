@@ -93,9 +93,6 @@ class CycleWorkspace:
         _lib.check(D.lib().mpk_dot(prec.code, b.shape[0], D.ptr(b), D.ptr(b), self.at(OFF_BN2),
                                    self.ws.ptr, D.stream()))
 
-    def clear_changed(self):
-        self.ctlbuf[OFF_CHANGED:OFF_CHANGED + 4].zero_()
-
     def cycle(self, A, M, r0, rnorm2_off, x0, x_out, steps_cap, exit_tol, norm_scale, rule, orth="cgs2"):
         """Enqueue one whole cycle (gmres.py:134-205) via mpk_cycle_run."""
         d = self.desc

@@ -10,6 +10,7 @@ import numpy as np
 import pytest
 
 import paper_2105_07544_b200 as mk
+from paper_2105_07544_b200 import _lib
 from paper_2105_07544_b200 import distributed as dd
 
 from conftest import random_csr
@@ -144,17 +145,53 @@ def test_lagged_cgs2_row_partitioned(cuda, P):
         try:
             inner = mk.SolverConfig(m=50, rtol=1e-4, precision=P32, max_iters=20000, orthogonalization="dcgs2")
             ir_rep = dd.dist_gmres_ir(sysm, b, np.zeros(A.n), mk.IrConfig(inner=inner, rtol=1e-10))
+            kern_ir = _lib.last_cycle_kernel()
             g64 = dd.dist_gmres_restarted(sysm, b, np.zeros(A.n),
                                           mk.SolverConfig(m=50, rtol=1e-10, orthogonalization="dcgs2"))
-            return ir_rep.total_iters, ir_rep.converged, g64.total_iters, g64.converged, g64.final_explicit_relres
+            kern64 = _lib.last_cycle_kernel()
+            return (ir_rep.total_iters, ir_rep.converged, g64.total_iters, g64.converged,
+                    g64.final_explicit_relres, kern_ir, kern64)
         finally:
             sysm.close()
 
     res = dd.run_virtual_ranks(P, fn)
     assert all(r == res[0] for r in res)
-    it_ir, c_ir, it64, c64, rel64 = res[0]
+    it_ir, c_ir, it64, c64, rel64, kern_ir, kern64 = res[0]
+    # the row-partitioned lagged kernel really ran (it used to fall back to CGS2)
+    assert kern_ir == "k_cycle_dcgs2/multi" and kern64 == "k_cycle_dcgs2/multi", (kern_ir, kern64)
     inner = mk.SolverConfig(m=50, rtol=1e-4, precision=P32, max_iters=20000, orthogonalization="dcgs2")
     ref_ir = mk.gmres_ir(A, b, np.zeros(A.n), mk.IrConfig(inner=inner, rtol=1e-10))
     ref64 = mk.gmres_restarted(A, None, b, np.zeros(A.n), mk.SolverConfig(m=50, rtol=1e-10, orthogonalization="dcgs2"))
     assert c_ir and c64 and rel64 <= 1e-10
     assert abs(it_ir - ref_ir.total_iters) <= 50 and abs(it64 - ref64.total_iters) <= 50
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_fp32_restarted_matches_single_gpu(cuda, P):
+    """fp32 row-partitioned GMRES(m) (e.g. GMRES-FD's low phase): the halo of
+    x comes from the fp32 peer set (it used to be read from an
+    fp64 buffer), with a nonzero x0 so the very first residual needs it."""
+    A = mk.convert_matrix(L("Laplace2D", 32), P32)
+    b = np.ones(A.n, np.float32)
+    x0 = (0.01 * np.sin(np.arange(A.n))).astype(np.float32)
+    cfg = mk.SolverConfig(m=30, rtol=1e-5, precision=P32, max_iters=3000)
+    ref = mk.gmres_restarted(A, None, b, x0, cfg)
+
+    def fn(comm):
+        sysm = dd.LocalSystem(comm, A)
+        try:
+            rep = dd.dist_gmres_restarted(sysm, b, x0, cfg)
+            return rep, rep.x.cpu().numpy(), (sysm.r0, sysm.r1)
+        finally:
+            sysm.close()
+
+    res = dd.run_virtual_ranks(P, fn)
+    rep = res[0][0]
+    assert rep.converged and ref.converged
+    assert abs(rep.total_iters - ref.total_iters) <= cfg.m
+    # the first explicit residual (x0's halo) is the single-GPU one to fp32 rounding
+    assert abs(rep.baseline - ref.baseline) <= 1e-5 * ref.baseline
+    x = np.zeros(A.n, np.float32)
+    for _, xl, (r0, r1) in res:
+        x[r0:r1] = xl
+    assert np.abs(x - ref.x).max() <= 1e-3 * np.abs(ref.x).max()
