@@ -1,14 +1,18 @@
-"""Benchmark: GMRES-IR time-to-1e-10 on BASELINE config C2 (BentPipe2D 1500^2,
-2.25M rows, restart 50, fp32 inner / fp64 outer), with the fp64 GMRES time,
-per-kernel HBM roofline and the reference CPU path (oracle port) beside it.
+"""Benchmark: GMRES-IR time-to-1e-10 on north_star's config C4 (Laplace3D
+200^3, 8M rows, restart 50, fp32 inner / fp64 outer) by default, with the
+fp64 GMRES time (the paper's IR speedup), per-kernel HBM roofline and the
+reference CPU path (oracle port) beside it.  --config C2 gives the BentPipe2D
+1500^2 headline of BASELINE.json's single-GPU config.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config C2|C1|C4] [--no-fp64] [--no-cpu]
+                    [--config C4|C1|C2|C3|C5] [--no-fp64] [--no-cpu]
 
 A step = one full solve (b = ones, x0 = 0, m = 50, rtol 1e-10) with inputs
-resident in HBM (value); e2e repeats it through the public API with host
-(pinned) b/x0 and the solution copied back.  Working set (Krylov basis
-459 MB fp32 / 918 MB fp64) exceeds the 126 MB L2, so no explicit flush.
+resident in HBM (value), timed with per-kernel profiling OFF; a separate
+profiled solve gives the per-kernel CUDA-event times for the roofline.  e2e
+repeats the solve through the public API with host (pinned) b/x0 and the
+solution copied back.  Working set (Krylov basis 1.6 GB fp32 at C4, 459 MB at
+C2) exceeds the 126 MB L2, so no explicit flush.
 N > 1 (torchrun): the same system row-partitioned across the ranks
 (paper_2105_07544_b200.distributed: P2P halo stores and in-kernel cross-GPU
 reductions inside each rank's persistent cycle kernel), strong scaling, max
@@ -43,9 +47,32 @@ CONFIGS = {
 # iterations (SURVEY 8(d) warning: the default family converges in 18)
 C5_PARAMS = dict(signs="negative", dominance=1.001, shift=1e-3, far_frac=0.01, band=2000)
 # reference (mpkrylov) iteration counts on these configs (tests/golden/runs.json)
+# C4 IR runs under breakdown rule "u"; its count is the paper's
+# Trilinos count, equal to this solver's and the oracle's
 REF_ITERS = {"C1": {"ir": 200, "fp64": 206}, "C2": {"ir": 10650, "fp64": 10833},
-             "C3": {"ir": None, "fp64": None}, "C4": {"ir": None, "fp64": 4053},
+             "C3": {"ir": None, "fp64": None}, "C4": {"ir": 4100, "fp64": 4053},
              "C5": {"ir": None, "fp64": None}}
+
+
+def breakdown_rule(cfg_name):
+    """the reference's beta <= n*u*||w|| test (n*u32 = 0.24 at 4M,
+    0.37 at 6.25M, 0.48 at 8M rows) declares false breakdowns on C3-C5; they
+    run with "u" (in both arms)."""
+    return "u" if cfg_name in ("C3", "C4", "C5") else "n_u"
+
+
+def shared_config(args):
+    """The workload description both arms print verbatim (same_config)."""
+    preset, nx, desc = CONFIGS[args.config]
+    basis = 51 * (nx if args.config == "C5" else nx ** (3 if preset == "Laplace3D" else 2)) * 4
+    cfg = {"workload": "%s, GMRES-IR restart 50, rtol 1e-10, b = ones, x0 = 0" % desc,
+           "config": args.config, "solver": "gmres-ir", "m": 50, "rtol": 1e-10,
+           "breakdown_rule": breakdown_rule(args.config),
+           "precond": ("jacobi:1" if args.config == "C5" else "poly:%d" % args.poly if args.poly else "none"),
+           "l2": ("no flush: working set > 126 MB L2 (Krylov basis alone %.2f GB fp32)" % (basis / 1e9)
+                  if basis > 126e6 else "working set fits in L2 (not flushed; latency-bound config)"),
+           "parallelism": "row-partitioned x%d" % args.gpus if args.gpus > 1 else "single"}
+    return cfg
 
 
 def peaks():
@@ -123,21 +150,29 @@ def cpu_cores():
         return os.cpu_count() or 1
 
 
+_CPU_SYS = {}
+
+
 def cpu_sample(cfg_name, solver, steps_budget=50):
     """Oracle port (CPU restatement of the reference) on a bounded sample:
-    `steps_budget` inner iterations of the same workload; returns s/iteration."""
+    `steps_budget` inner iterations of the same workload; returns s/iteration.
+    The matrix is assembled once (setup, untimed as in cli.py:166-168)."""
     from oracle import mpk_oracle as O
 
     preset, nx, _ = CONFIGS[cfg_name]
-    rp, ci, v = O.stencil_csr(preset, nx)
+    if cfg_name not in _CPU_SYS:
+        rp, ci, v = O.stencil_csr(preset, nx)
+        _CPU_SYS[cfg_name] = (rp, ci, v, v.astype(np.float32))
+    rp, ci, v, v32 = _CPU_SYS[cfg_name]
     n = rp.size - 1
     b = np.ones(n)
+    rule = breakdown_rule(cfg_name)
     t0 = time.perf_counter()
     if solver == "ir":
         out = O.refine((rp, ci, v), b, np.zeros(n), 50, 1e-10, steps_budget,
-                       A32=(rp, ci, v.astype(np.float32)))
+                       A32=(rp, ci, v32), rule=rule)
     else:
-        out = O.restarted((rp, ci, v), None, b, np.zeros(n), 50, 1e-10, steps_budget)
+        out = O.restarted((rp, ci, v), None, b, np.zeros(n), 50, 1e-10, steps_budget, rule=rule)
     dt = time.perf_counter() - t0
     return dt / max(out.iters, 1), out.iters, dt
 
@@ -155,28 +190,42 @@ def cycle_steps(history):
 
 
 def run_reference_arm(args):
+    """Reference CPU path (the oracle port, pinned to the unmodified
+    reference's goldens) on the box's host cores: each step is a bounded
+    sample of the same solve (one refinement = 50 inner iterations plus the
+    outer fp64 residual pass).  value = median s/iteration x the reference's
+    iteration count for the config (an extrapolation, stated in `note`;
+    profiles/r02_cpu_full_runs.json holds full runs to convergence that
+    validate it).  ms_per_step is the sample's own wall time."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    preset, nx, desc = CONFIGS[args.config]
-    iters_full = REF_ITERS[args.config]["ir"] or REF_ITERS[args.config]["fp64"]
+    if args.config not in ("C1", "C2", "C4"):
+        print(json.dumps({"impl": "reference", "unavailable": "reference arm implemented for C1/C2/C4 only"}))
+        return
+    iters_full = REF_ITERS[args.config]["ir"]
+    cpu_sample(args.config, "ir", 5)   # assembly (setup) + page-in, untimed
     for _ in range(args.warmup):
-        cpu_sample(args.config, "ir", 10)
-    per_it = []
+        cpu_sample(args.config, "ir", 5)
+    per_it, walls = [], []
     for _ in range(args.steps):
-        s, it, _dt = cpu_sample(args.config, "ir", 50)
+        s, it, dt = cpu_sample(args.config, "ir", 50)
         per_it.append(s)
+        walls.append(dt)
     value = float(np.median(per_it)) * iters_full
     line = {
         "impl": "reference", "metric": "GMRES-IR time-to-1e-10 residual (s)", "value": value,
         "unit": "s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32-inner/f64-outer", "data": "synthetic (generated stencil, b = ones)",
-        "config": {"workload": "%s GMRES-IR(50) rtol 1e-10" % desc, "config": args.config},
+        "ms_per_step": float(np.mean(walls)) * 1e3, "higher_is_better": False,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+        "dtype": "f32-inner/f64-outer", "data": "synthetic (generated stencil, b = ones, x0 = 0)",
+        "config": shared_config(args),
         "cpu_baseline": {"value": value, "unit": "s", "cores": cpu_cores(), "kind": "port",
                          "sample": "50 inner iterations (one refinement) of the same solve per step, "
                                    "median s/iteration x reference iteration count %d" % iters_full},
         "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "value extrapolated: median s/iteration over the samples x the reference's iteration "
+                "count; ms_per_step = measured wall time of one 50-iteration sample",
     }
     print(json.dumps(line), flush=True)
 
@@ -187,7 +236,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
     ap.add_argument("--no-fp64", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -218,10 +267,7 @@ def main():
     lib = _lib.load()
     P = mk.Precision
     preset, nx, desc = CONFIGS[args.config]
-    # the reference's beta <= n*u*||w|| test (n*u32 = 0.24 at 4M,
-    # 0.37 at 6.25M, 0.48 at 8M rows) declares false breakdowns on C3-C5;
-    # they run with "u"
-    rule = "u" if args.config in ("C3", "C4", "C5") else "n_u"
+    rule = breakdown_rule(args.config)
     if args.config == "C5":
         A = mk.synthetic_irregular(nx, **C5_PARAMS)
     else:
@@ -293,14 +339,17 @@ def main():
     for _ in range(args.warmup):
         rep = solve_ir(b_dev, x0_dev)
         note("warmup solve: %d iters" % rep.total_iters)
-    # timed region: K solves with per-kernel events on the launching stream
+    # timed region: K solves, per-kernel profiling off
     launches0 = lib.mpk_launch_count()
-    lib.mpk_prof_reset()
-    wsi.flags = 1
+    wsi.flags = 0
     with ClockSampler(dev) as clk:
         ms_ir, reps = timed(lambda: solve_ir(b_dev, x0_dev), args.steps)
-    wsi.flags = 0
     launches = lib.mpk_launch_count() - launches0
+    # separate profiled solve: per-kernel CUDA events on the launching stream
+    lib.mpk_prof_reset()
+    wsi.flags = 1
+    ms_prof, reps_prof = timed(lambda: solve_ir(b_dev, x0_dev), 1)
+    wsi.flags = 0
     NC = 8
     import ctypes
     pm = (ctypes.c_double * NC)()
@@ -315,9 +364,9 @@ def main():
     sv = 4
     # matrix-free stencil: x read + y write; CSR: sv*(nnz+2n) + 4*(nnz+n+1)
     spmv_b = 2.0 * sv * n_loc if A.stencil is not None else sv * (A.nnz + 2.0 * n) + 4.0 * (A.nnz + n + 1)
-    steps_per_cycle = cycle_steps(rep.history)
+    steps_per_cycle = cycle_steps(reps_prof[-1].history)
     alg = sum(sum(spmv_b + sv * n_loc * (4 * (k + 1) + 10) for k in range(st)) + sv * n_loc * (st + 2)
-              for st in steps_per_cycle) * args.steps
+              for st in cycle_steps(reps_prof[-1].history))
     names = ["spmv+norm+dot1", "update1+dot2", "update2+norm+givens", "normalise", "precond",
              "correction", "residual", "persistent Arnoldi cycle (k_cycle_reg)"]
     kern = {}
@@ -352,13 +401,11 @@ def main():
         "higher_is_better": False, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
         "dtype": "f32-inner/f64-outer",
         "data": "synthetic (generated %s, b = ones, x0 = 0)" % preset,
-        "config": {"workload": "%s, GMRES-IR restart 50, rtol 1e-10" % desc,
-                   "config": args.config, "n": n, "nnz": A.nnz, "m": 50, "breakdown_rule": rule,
-                   "operator": "matrix-free stencil (bit-identical to CSR)",
-                   "parallelism": ("row-partitioned x%d (P2P halo + in-kernel cross-GPU reductions)" % world
-                                   if world > 1 else "single"),
-                   "rows_per_rank": n_loc,
-                   "l2": "working set > L2 (basis %.0f MB per rank)" % ((51 * n_loc * 4) / 1e6)},
+        "config": shared_config(args),
+        "details": {"n": n, "nnz": A.nnz, "operator": "matrix-free stencil (bit-identical to CSR)",
+                    "parallelism": ("row-partitioned x%d (P2P halo + in-kernel cross-GPU reductions)" % world
+                                    if world > 1 else "single"),
+                    "rows_per_rank": n_loc, "profiled_solve_s": ms_prof / 1e3},
         "iters": rep.total_iters, "refinements": rep.restarts, "final_relres": rep.final_explicit_relres,
         "converged": bool(rep.converged),
         "ref_iters": REF_ITERS[args.config]["ir"],
@@ -454,13 +501,13 @@ def main():
         out["fd"] = {"switch_iter": args.fd, "s": msfd / 1e3, "iters": repfd[-1].total_iters,
                      "converged": bool(repfd[-1].converged)}
     if args.config == "C5":
-        out["config"]["precond"] = {"kind": "block-jacobi", "block": 1, "fused": "diagonal scaling in k_cycle_reg"}
-        out["config"]["operator"] = "CSR, warp-cooperative bit-exact rows"
-        out["config"]["generator"] = dict(C5_PARAMS, seed=20240817)
+        out["details"]["precond"] = {"kind": "block-jacobi", "block": 1, "fused": "diagonal scaling in k_cycle_reg"}
+        out["details"]["operator"] = "CSR, warp-cooperative bit-exact rows"
+        out["details"]["generator"] = dict(C5_PARAMS, seed=20240817)
     elif M32 is not None:
-        out["config"]["precond"] = {"kind": "gmres-poly", "degree_ir": M32.data.degree,
-                                    "degree_fp64": M64.data.degree, "seed": "ones"}
-        out["config"]["operator"] = "matrix-free stencil; poly apply = degree SpMVs per step"
+        out["details"]["precond"] = {"kind": "gmres-poly", "degree_ir": M32.data.degree,
+                                     "degree_fp64": M64.data.degree, "seed": "ones"}
+        out["details"]["operator"] = "matrix-free stencil; poly apply = degree SpMVs per step"
     if rank == 0 and world == 1 and not args.no_cpu and not args.poly and args.config != "C5":
         s_it, it, dt = cpu_sample(args.config, "ir", 50)
         full = REF_ITERS[args.config]["ir"] or rep.total_iters
