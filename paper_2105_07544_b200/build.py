@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "_lib", "libmpkb200.so")
 SOURCES = ["abi.cu", "host_rcm.cpp"]
-DEPS = ["abi.cu", "host_rcm.cpp", "fused.cuh", "fused_reg.cuh", "fused_dcgs2.cuh", "tma.cuh", "kernels.cuh", "ops.cuh", "common.cuh", "../../include/mpk_b200.h"]
+DEPS = ["abi.cu", "host_rcm.cpp", "fused.cuh", "fused_reg.cuh", "fused_dcgs2.cuh", "tma.cuh", "kernels.cuh", "ops.cuh", "common.cuh", "comm.cuh", "../../include/mpk_b200.h"]
 
 
 def nvcc() -> str:
@@ -41,6 +41,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-o", OUT + ".tmp"] + [os.path.join(SRC, s) for s in SOURCES]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
+    if os.environ.get("MPK_SPLIT_COMPILE"):
+        # development builds only: parallel cicc/ptxas changes code generation
+        # (measured: different stack frames), so shipped builds never use it
+        cmd.insert(1, "--split-compile=%s" % os.environ["MPK_SPLIT_COMPILE"])
     subprocess.run(cmd, check=True)
     os.replace(OUT + ".tmp", OUT)
     return OUT
