@@ -1,0 +1,89 @@
+"""Parity at BASELINE scale (VERDICT r1 "Next round" 1): full C2 / C4 solves
+on the GPU against runs of the UNMODIFIED reference at the same size
+(tests/golden/runs.json["ir_bp1500"], tests/golden/big/*.npz, made by
+tests/golden/make_golden.py --big and tests/golden/make_big_golden.py).
+
+What the reference itself pins, and what these tests hold:
+
+* Restarted GMRES over hundreds of cycles is chaotic in the last bit: the
+  reference's own C2 fp64 count moves with the OpenBLAS thread count
+  (10504 at 4 threads, 10833 at 8), and this solver's moves
+  with the reduction order (10438-10913 for 148/144/128/100/74 CTAs,
+  profiles/r02_C2_fp64_spread.json).  Every pair of runs -- reference vs
+  GPU, or GPU vs GPU with another CTA count -- agrees to ~1e-13 for the
+  first ~37 cycles and then diverges exponentially.  So the tests pin
+  (a) the histories to rounding over the pre-chaotic window, (b) the
+  trajectories to a bounded band over the whole solve, and (c) the counts
+  to the reference's spread widened by one restart cycle.
+"""
+
+import glob
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2105_07544_b200 as mk
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+P = mk.Precision
+
+
+def explicit(rep, phase):
+    return np.array([e.explicit_relres for e in rep.history if e.phase == phase and e.explicit_relres is not None])
+
+
+def big(case):
+    """Reference runs of `case` at every recorded BLAS thread count."""
+    return [np.load(f) for f in sorted(glob.glob(os.path.join(GOLD, "big", case + "_t*.npz")))]
+
+
+@pytest.fixture(scope="module")
+def bentpipe():
+    return mk.generate_stencil(mk.ProblemSpec("BentPipe2D", 1500))
+
+
+def test_c2_gmres_ir_matches_reference_run(bentpipe):
+    """C2 GMRES-IR(50) vs the reference's full run (710 s of CPU)."""
+    ref = json.load(open(os.path.join(GOLD, "runs.json")))["ir_bp1500"]
+    A = bentpipe
+    inner = mk.SolverConfig(m=50, rtol=1e-4, precision=P.binary32, max_iters=100000)
+    rep = mk.gmres_ir(A, np.ones(A.n), np.zeros(A.n), mk.IrConfig(inner=inner, rtol=1e-10))
+    assert rep.converged and rep.final_explicit_relres <= 1e-10
+    assert abs(rep.total_iters - ref["iters"]) <= 50, (rep.total_iters, ref["iters"])
+    assert abs(rep.restarts - ref["restarts"]) <= 1
+    ours = explicit(rep, "outer")
+    theirs = np.array([r[3] for r in ref["history"] if r[1] == "outer"])
+    k = min(len(ours), len(theirs))
+    rel = np.abs(ours[:k] / theirs[:k] - 1)
+    # fp32 inner cycles: the first 30 refinements agree to 1e-6 (observed 2.3e-7)
+    assert rel[:30].max() <= 1e-6, rel[:30].max()
+    # then the fp32 trajectories drift apart but stay within a factor 10^0.5
+    # of each other (observed max 0.34 decades)
+    assert np.abs(np.log10(ours[:k] / theirs[:k])).max() <= 0.5
+
+
+def test_c2_fp64_gmres_matches_reference_runs(bentpipe):
+    """C2 fp64 GMRES(50) vs the reference's full runs (20 min of CPU each)."""
+    runs = big("c2_fp64")
+    assert runs, "missing tests/golden/big/c2_fp64_t*.npz"
+    A = bentpipe
+    rep = mk.gmres_restarted(A, None, np.ones(A.n), np.zeros(A.n), mk.SolverConfig(m=50, rtol=1e-10,
+                                                                                   max_iters=100000))
+    assert rep.converged and rep.final_explicit_relres <= 1e-10
+    ours = np.array([e.explicit_relres for e in rep.history if e.explicit_relres is not None])
+    impl = np.array([np.nan if e.implicit_relres is None else e.implicit_relres for e in rep.history])
+    for g in runs:
+        theirs = g["h_expl"][~np.isnan(g["h_expl"])]
+        # pre-chaotic window: 36 restart cycles (1800 iterations) to 1e-11
+        # relative (observed 3.4e-13), implicit residuals to 1e-12 (7e-14)
+        assert np.abs(ours[:37] / theirs[:37] - 1).max() <= 1e-11
+        gi = g["h_impl"][:1800]
+        m = ~np.isnan(gi) & ~np.isnan(impl[:1800])
+        assert np.abs(impl[:1800][m] / gi[m] - 1).max() <= 1e-12
+        k = min(len(ours), len(theirs))
+        assert np.abs(np.log10(ours[:k] / theirs[:k])).max() <= 0.5   # observed 0.29 decades
+    counts = [int(g["iters"]) for g in runs] + [10833]   # + SURVEY §6 (8 threads)
+    assert min(counts) - 100 <= rep.total_iters <= max(counts) + 100, (rep.total_iters, counts)
