@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define MPK_ABI_VERSION 1
+#define MPK_ABI_VERSION 2   /* 2: mpk_matrix.band */
 
 /* storage precision (precision.py:14-71: binary32 / binary64) */
 enum { MPK_F32 = 0, MPK_F64 = 1 };
@@ -75,6 +75,8 @@ typedef struct mpk_matrix {
     int32_t nx;
     int64_t row0;
     double diffusion, velocity, convection, stretch;
+    int64_t band;       /* CSR only: x-window half-width for banded rows (0 = off);
+                           the caller sets it from row statistics (sparse.py) */
 } mpk_matrix;
 
 /*
@@ -246,7 +248,10 @@ typedef struct mpk_cycle_desc {
     int32_t flags;          /* bit0: per-kernel event timing; bit1: write the last basis column;
                                bit2: force the multi-kernel cycle (no persistent kernel);
                                bit3: phase profiler of the persistent kernel;
-                               bit4: lagged one-reduction CGS2 (identity preconditioner, m <= 51) */
+                               bit4: lagged one-reduction CGS2 (identity preconditioner, m <= 51);
+                               bit5: basis stored in binary16 (scaled by a power of two; binary32
+                                     cycles, one GPU, m <= 51, CGS2, identity or Jacobi(1)); V then
+                                     holds ld * (m + 1) binary16 values */
     const mpk_comm *comm;   /* nranks > 1: this rank's view of the communicator */
 } mpk_cycle_desc;
 
@@ -287,6 +292,18 @@ int mpk_ir_update(int64_t n, double *x, const float *u, int32_t *changed, void *
 /* preconditioner application (preconditioners.py:133-139, 276-305)    */
 /* ------------------------------------------------------------------ */
 int mpk_precond_apply(const mpk_precond *M, const void *v, void *out, void *stream);
+
+/*
+ * Block-Jacobi setup on the device (replaces build_block_jacobi's per-block
+ * scipy.linalg.lu_factor loop, pkg/src/mpkrylov/preconditioners.py:96-130):
+ * dense k-by-k diagonal blocks of the CSR matrix A (its dtype), LU with
+ * partial pivoting, factors in mpk_precond's JACOBI layout (lu: nblocks*k*k,
+ * piv: nblocks*k).  minpiv[b] = min|u_ii| (A's dtype), thr[b] = (kb*u)*max
+ * row sum |a| (double); *bad (initialise to INT32_MAX) = the lowest block with
+ * minpiv <= thr (the reference's SingularBlockError).  1 <= k <= 64.
+ */
+int mpk_block_lu(const mpk_matrix *A, int32_t k, void *lu, int32_t *piv, void *minpiv, double *thr, int32_t *bad,
+                 void *stream);
 
 /* ------------------------------------------------------------------ */
 /* host-side setup                                                     */

@@ -429,8 +429,21 @@ class CycleOut:
     breakdown: bool
 
 
-def one_cycle(A, M, b, x0, m, tol, r0=None, scale=None, cap=None, rule="n_u"):
-    """gmres_cycle (gmres.py:134-205). A = (rp, ci, vals); M callable or None."""
+def basis16_scale(n):
+    """Power-of-two scale of the binary16 basis: 2^round(log2(sqrt(n)))."""
+    return float(2.0 ** np.rint(0.5 * np.log2(max(n, 1))))
+
+
+def round16(v, s):
+    """Stored value of a binary16 basis entry: half(v*s) read back as v' = half/s
+    (this repo's third precision, SolverConfig.basis_precision; not in the
+    reference -- PAPER.md:441 future work)."""
+    return ((v * np.float32(s)).astype(np.float16).astype(np.float32) / np.float32(s)).astype(v.dtype)
+
+
+def one_cycle(A, M, b, x0, m, tol, r0=None, scale=None, cap=None, rule="n_u", basis16=False):
+    """gmres_cycle (gmres.py:134-205). A = (rp, ci, vals); M callable or None.
+    basis16: store the basis columns rounded to binary16 (round16)."""
     rp, ci, vals = A
     dt = vals.dtype
     Mf = M if M is not None else (lambda v: v)
@@ -443,8 +456,9 @@ def one_cycle(A, M, b, x0, m, tol, r0=None, scale=None, cap=None, rule="n_u"):
     if float(gam) == 0.0:
         return x0.copy(), CycleOut(0, [], sc if sc > 0 else 1.0, False)
     n = b.shape[0]
+    s16 = basis16_scale(n)
     V = np.zeros((n, steps_cap + 1), dtype=dt, order="F")
-    V[:, 0] = r / gam
+    V[:, 0] = round16(r / gam, s16) if basis16 else r / gam
     cnt = 1
     lsq = RotatedLsq(steps_cap, gam, sc, dt)
     rels = []
@@ -454,7 +468,7 @@ def one_cycle(A, M, b, x0, m, tol, r0=None, scale=None, cap=None, rule="n_u"):
         w = spmv_seq(rp, ci, vals, Mf(V[:, k]))
         coeffs, beta, ok, q = cgs2_step(V, cnt, w, rule)
         if ok:
-            V[:, cnt] = q
+            V[:, cnt] = round16(q, s16) if basis16 else q
             cnt += 1
         rel = lsq.push(coeffs, beta)
         rels.append(rel)
@@ -515,7 +529,7 @@ def restarted(A, M, b, x0, m=50, rtol=1e-10, max_iters=100_000, max_restarts=1_0
 
 
 def refine(A64, b, x0, m=50, rtol=1e-10, inner_max_iters=100_000, max_refinements=1_000_000,
-           M=None, A32=None, rule="n_u"):
+           M=None, A32=None, rule="n_u", basis16=False):
     """gmres_ir (multiprecision.py:120-233): fp64 outer, fp32 inner cycles."""
     rp, ci, v64 = A64
     if A32 is None:
@@ -551,7 +565,7 @@ def refine(A64, b, x0, m=50, rtol=1e-10, inner_max_iters=100_000, max_refinement
                 stalled = True
                 break
             continue
-        u32, st = one_cycle(A32, M, r32, z32, m, floor, r0=r32, cap=left, rule=rule)
+        u32, st = one_cycle(A32, M, r32, z32, m, floor, r0=r32, cap=left, rule=rule, basis16=basis16)
         hist.extend((total + i + 1, "inner", rel * r32n / base, None)
                     for i, rel in enumerate(st.implicit))
         total += st.steps

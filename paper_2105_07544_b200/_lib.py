@@ -30,6 +30,7 @@ EXPORTS = (
     "mpk_lsq_solve", "mpk_vdiv", "mpk_launch_count", "mpk_fused_prof_read", "mpk_comm_part_bytes",
     "mpk_dev_alloc", "mpk_dev_free", "mpk_ipc_get", "mpk_ipc_open", "mpk_ipc_close", "mpk_rcm_host",
     "mpk_last_cycle_kernel", "mpk_can_access_peer", "mpk_comm_push_rows", "mpk_comm_reduce_ctl",
+    "mpk_block_lu",
 )
 MAX_RANKS = 8
 
@@ -38,13 +39,16 @@ class NativeUnavailable(RuntimeError):
     """The sm_100a library (or a CUDA device) is not available."""
 
 
+ABI_VERSION = 2   # include/mpk_b200.h MPK_ABI_VERSION
+
+
 class MpkMatrix(ctypes.Structure):
     _fields_ = [
         ("kind", ctypes.c_int32), ("dtype", ctypes.c_int32), ("n", ctypes.c_int64),
         ("nnz", ctypes.c_int64), ("row_ptr", ctypes.c_void_p), ("col_idx", ctypes.c_void_p),
         ("values", ctypes.c_void_p), ("preset", ctypes.c_int32), ("nx", ctypes.c_int32),
         ("row0", ctypes.c_int64), ("diffusion", ctypes.c_double), ("velocity", ctypes.c_double),
-        ("convection", ctypes.c_double), ("stretch", ctypes.c_double),
+        ("convection", ctypes.c_double), ("stretch", ctypes.c_double), ("band", ctypes.c_int64),
     ]
 
 
@@ -134,6 +138,7 @@ _SIGS["mpk_vdiv"] = (_I32, [_I32, _I64, _P, _P, _P, _P])
 _SIGS["mpk_lsq_init"] = (_I32, [_I32, _I32, ctypes.c_double, ctypes.c_double, _P, _P, _P])
 _SIGS["mpk_lsq_update"] = (_I32, [_I32, _I32, _I32, _P, _P, _P, _P, _P, _P])
 _SIGS["mpk_lsq_solve"] = (_I32, [_I32, _I32, _I32, _P, _P, _P])
+_SIGS["mpk_block_lu"] = (_I32, [ctypes.POINTER(MpkMatrix), _I32, _P, _P, _P, _P, _P, _P])
 
 
 def load(require_device: bool = True):
@@ -148,6 +153,9 @@ def load(require_device: bool = True):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
+        if lib.mpk_abi_version() != ABI_VERSION:
+            raise NativeUnavailable("libmpkb200.so has ABI %d, this package needs %d: rebuild it"
+                                    % (lib.mpk_abi_version(), ABI_VERSION))
         _LIB = lib
     if require_device:
         import torch

@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "_lib", "libmpkb200.so")
 SOURCES = ["abi.cu", "host_rcm.cpp"]
-DEPS = ["abi.cu", "host_rcm.cpp", "fused.cuh", "fused_reg.cuh", "fused_dcgs2.cuh", "tma.cuh", "kernels.cuh", "ops.cuh", "common.cuh", "comm.cuh", "../../include/mpk_b200.h"]
+DEPS = ["abi.cu", "host_rcm.cpp", "fused.cuh", "fused_reg.cuh", "fused_dcgs2.cuh", "kernels.cuh", "ops.cuh", "common.cuh", "comm.cuh", "../../include/mpk_b200.h"]
 
 
 def nvcc() -> str:

@@ -3,11 +3,10 @@
 // runtime of one restarted-GMRES cycle: it enqueues every kernel of the
 // cycle on the caller's stream without synchronising; early exits are
 // device-side (ctl->done), so the host reads back once per cycle.
-#include <cuda.h>
-#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -62,14 +61,18 @@ int max_blocks() { return sm_count_cached() * kMaxBlocksPerSm; }
 template <class K> int grid_for(K kernel, size_t smem, int64_t n) {
     static std::mutex mu;
     static std::map<std::pair<const void *, size_t>, int> occ;
+    static std::map<const void *, size_t> attr;   // dynamic shared memory opted in per kernel (only raised)
     int per_sm;
     {
         std::lock_guard<std::mutex> lk(mu);
+        size_t &have = attr[(const void *)kernel];
+        if (smem > have) {
+            cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            have = smem;
+        }
         auto key = std::make_pair((const void *)kernel, smem);
         auto it = occ.find(key);
         if (it == occ.end()) {
-            if (smem > 48 * 1024)
-                cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             int o = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kernel, kBlock, smem);
             if (o < 1) o = 1;
@@ -258,7 +261,21 @@ template <typename T> CsrOp<T> make_csr(const mpk_matrix *A) {
     op.rp = A->row_ptr;
     op.ci = A->col_idx;
     op.v = (const T *)A->values;
+    op.band = (A->band > 0 && A->row0 == 0) ? A->band : 0;   // windows only on whole (one-GPU) matrices
+    op.nnz_ = A->nnz;
     return op;
+}
+
+// Shared-memory x window of a banded CSR chunk: `rows` + 2*band elements,
+// or 0 when the rows are short (<= 16 entries on average: their gathers hit
+// L1, and the window costs occupancy -- C2's 5-entry rows ran 1.8x slower
+// with it), the matrix is not banded, or the window would not fit.
+constexpr int64_t kWinMaxBytes = 96 * 1024;
+template <typename T> int64_t csr_window_elems(const CsrOp<T> &op, int64_t rows) {
+    if (op.band <= 0 || op.n <= 0) return 0;
+    if ((int64_t)op.nnz_ <= 16 * op.n) return 0;
+    const int64_t e = rows + 2 * op.band;
+    return e * (int64_t)sizeof(T) <= kWinMaxBytes ? e : 0;
 }
 
 template <typename T, class F> int with_op(const mpk_matrix *A, F &&f) {
@@ -496,103 +513,6 @@ int apply_precond(const mpk_precond *M, const T *v, T *out, const int32_t *done,
 // ---------------------------------------------------------------------------
 // one GMRES cycle
 // ---------------------------------------------------------------------------
-// 2-D tensor map of a column-major basis V (ld rows x ncols columns) with
-// TR x kCB boxes; out-of-range rows/columns read as zero.
-int encode_basis_map(CUtensorMap *map, const void *V, int64_t ld, int ncols, int sv, int TR) {
-    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
-    if (!enc) {
-        cudaDriverEntryPointQueryResult q;
-        void *fn = nullptr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
-            return fail(MPK_ELAUNCH, "cuTensorMapEncodeTiled unavailable");
-        enc = (PFN_cuTensorMapEncodeTiled_v12000)fn;
-    }
-    cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)ncols};
-    cuuint64_t strides[1] = {(cuuint64_t)ld * sv};
-    cuuint32_t box[2] = {(cuuint32_t)TR, (cuuint32_t)kCB};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = enc(map, sv == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
-                     const_cast<void *>(V), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return fail(MPK_ELAUNCH, "cuTensorMapEncodeTiled failed");
-    return MPK_OK;
-}
-
-// Rows per TMA tile of the fused cycle (64, 128 or 256): 512 bytes of each
-// column per tile by default (128 fp32 / 64 fp64 rows; a 51-column stage is
-// ~33 KB, so the ring keeps 4-5 stages in flight).  MPK_FUSED_TR overrides.
-int fused_tile_rows(int sv) {
-    static int rows = -1;
-    if (rows < 0) {
-        const char *e = getenv("MPK_FUSED_TR");
-        rows = e ? atoi(e) : 0;
-        if (rows != 64 && rows != 128 && rows != 256) rows = 0;
-    }
-    return rows ? rows : 512 / sv;
-}
-
-template <typename T, class Op, int TR>
-int launch_fused(const Op &op, const mpk_cycle_desc *d, int cap, double tf, double u, cudaStream_t s) {
-    static_assert(TR <= kMaxTR, "tile rows");
-    const int m = d->m;
-    T *w = (T *)d->work;
-    Ws ws = carve(d->ws);
-    auto kern = k_cycle_fused<T, Op, TR>;
-    const size_t smem = (size_t)kRingBytes + 8 * kMaxStages +
-                        sizeof(T) * ((size_t)(m + 1) * m + 2 * m + (m + 1) + 2 * kFSlots + kFB + kMaxTR + kFW);
-    CUtensorMap tmap;
-    int erc = encode_basis_map(&tmap, d->V, d->ld, m + 1, (int)sizeof(T), TR);
-    if (erc) return erc;
-    static size_t attr_set = 0;
-    if (smem > attr_set) {
-        cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (ea != cudaSuccess) {
-            g_err = std::string("k_cycle_fused smem attribute: ") + cudaGetErrorString(ea);
-            return MPK_ELAUNCH;
-        }
-        attr_set = smem;
-    }
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFB, smem);
-    if (per_sm < 1) return fail(MPK_ELAUNCH, "fused cycle kernel does not fit on an SM");
-    int grid = sm_count_cached();
-    if (grid > kFMaxCtas) grid = kFMaxCtas;
-    FusedArgs<T> fa;
-    fa.n = d->n;
-    fa.ld = d->ld;
-    fa.m = m;
-    fa.cap = cap;
-    fa.V = (T *)d->V;
-    fa.r0 = (const T *)d->r0;
-    fa.rnorm2 = (const T *)d->rnorm2;
-    fa.x0 = (const T *)d->x0;
-    fa.x_out = (T *)d->x_out;
-    fa.w = w;
-    fa.wp = w + d->ld;
-    fa.wpp = w + 2 * d->ld;
-    fa.part = (T *)ws.partials;
-    fa.bar = ws.counters + 8;
-    fa.H = hess_view<T>(d->hess, m);
-    fa.ctl = d->ctl;
-    fa.tf = tf;
-    fa.exit_tol = d->exit_tol;
-    fa.norm_scale = d->norm_scale;
-    fa.u = u;
-    fa.final_col = (d->flags & 2) ? 1 : 0;
-    fa.prof = (d->flags & 8) ? 1 : 0;
-    Op opc = op;
-    void *args[] = {(void *)&opc, (void *)&fa, (void *)&tmap};
-    ProfScope ps(7, 0.0, s);
-    cudaError_t e = cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(kFB), args, smem, s);
-    if (e != cudaSuccess) {
-        g_err = std::string("k_cycle_fused: ") + cudaGetErrorString(e);
-        return MPK_ELAUNCH;
-    }
-    g_last_cycle = "k_cycle_fused";
-    return check_launch("k_cycle_fused");
-}
-
 int64_t comm_part_core(int32_t dtype) { return 3LL * kFSlots * kXStride * (dtype == MPK_F64 ? 8 : 4); }
 
 // the per-restart collectives' view of a communicator (comm.cuh); `dtype` =
@@ -615,17 +535,6 @@ int comm_view(const mpk_comm *c, int32_t dtype, CommView &v) {
         v.mir_hi[q] = c->mir_hi[q];
     }
     return MPK_OK;
-}
-
-// Persistent cycle variant: "reg" (16-byte register streaming, default) or
-// "tma" (TMA ring through shared memory); MPK_FUSED_IMPL overrides.
-bool fused_use_tma() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("MPK_FUSED_IMPL");
-        v = (e && strcmp(e, "tma") == 0) ? 1 : 0;
-    }
-    return v == 1;
 }
 
 // CTAs of the persistent cycle: one per SM, at least 64 rows each
@@ -677,7 +586,10 @@ template <typename T> int fill_comm(FusedArgs<T> &fa, const mpk_cycle_desc *d, i
     return MPK_OK;
 }
 
-template <typename T, class Op>
+// k_cycle_reg launch; TV = __half stores the basis in binary16 (desc flag
+// bit 5: fp32 cycles on one GPU, m <= 51), scaled by vs = 2^round(log2
+// sqrt(n)) so normalised basis entries sit in binary16's normal range.
+template <typename T, class Op, typename TV = T>
 int launch_fused_reg(const Op &op, const mpk_cycle_desc *d, int cap, double tf, double u, cudaStream_t s) {
     const int m = d->m;
     T *w = (T *)d->work;
@@ -685,13 +597,20 @@ int launch_fused_reg(const Op &op, const mpk_cycle_desc *d, int cap, double tf, 
     // layout of k_cycle_reg: small m keeps R (m+1 x m) in shared memory
     const bool big = m + 1 > kRegMaxCols;
     const bool multi = d->nranks > 1;
+    constexpr bool half = !std::is_same<T, TV>::value;
     if (multi && big) return fail(MPK_EUNSUPPORTED, "row-partitioned cycles support m <= 51");
-    auto kern = multi ? k_cycle_reg<T, Op, false, true>
+    if (half && (multi || big)) return fail(MPK_EUNSUPPORTED, "binary16 basis: one GPU, m <= 51");
+    void (*kern)(Op, FusedArgs<T>);
+    if constexpr (half) kern = k_cycle_reg<T, Op, false, false, TV>;
+    else kern = multi ? k_cycle_reg<T, Op, false, true>
                       : (big ? k_cycle_reg<T, Op, true, false> : k_cycle_reg<T, Op, false, false>);
     const size_t nslot = big ? (size_t)m + 2 : (size_t)kFSlots;
+    int64_t win = 0;   // banded CSR: x window of phase A's SpMV chunks
+    if constexpr (!Op::kStencil)
+        if (!multi) win = csr_window_elems(op, kRegCsrChunk);
     const size_t smem = sizeof(T) * ((big ? 0 : (size_t)(m + 1) * m) + 2 * m + (m + 1) + 2 * nslot + kFW * kFSlots +
-                                     (big ? nslot : 0) + kFW * kCsrWarpBuf);
-    static size_t attr_set[3] = {0, 0, 0};
+                                     (big ? nslot : 0) + kFW * kCsrWarpBuf + (size_t)win);
+    static size_t attr_set[3] = {0, 0, 0};   // per instantiation (TV is a template parameter)
     const int vi = multi ? 2 : (big ? 1 : 0);
     if (smem > attr_set[vi]) {
         cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -732,6 +651,12 @@ int launch_fused_reg(const Op &op, const mpk_cycle_desc *d, int cap, double tf, 
     fa.prof = (d->flags & 8) ? 1 : 0;
     fa.diag = nullptr;
     fa.z = w + 3 * d->ld;
+    fa.csr_win = win > 0 ? 1 : 0;
+    if constexpr (half) {
+        const double e = std::nearbyint(0.5 * std::log2((double)(d->n > 1 ? d->n : 1)));
+        fa.vs = (T)std::ldexp(1.0, (int)e);
+        fa.vsi = (T)std::ldexp(1.0, -(int)e);
+    }
     if (d->M && d->M->kind == MPK_PC_JACOBI && d->M->block == 1 && d->M->dtype == d->dtype)
         fa.diag = (const T *)d->M->lu;
     if (int rc = fill_comm<T>(fa, d, grid)) return rc;
@@ -743,7 +668,7 @@ int launch_fused_reg(const Op &op, const mpk_cycle_desc *d, int cap, double tf, 
         g_err = std::string("k_cycle_reg: ") + cudaGetErrorString(e);
         return MPK_ELAUNCH;
     }
-    g_last_cycle = multi ? "k_cycle_reg/multi" : (big ? "k_cycle_reg/big" : "k_cycle_reg");
+    g_last_cycle = half ? "k_cycle_reg/half" : multi ? "k_cycle_reg/multi" : (big ? "k_cycle_reg/big" : "k_cycle_reg");
     return check_launch("k_cycle_reg");
 }
 
@@ -845,40 +770,41 @@ template <typename T> int run_cycle(const mpk_cycle_desc *d, cudaStream_t s) {
     // register kernel applies it inside its SpMV input and correction
     const bool diag1 = precond && d->M->kind == MPK_PC_JACOBI && d->M->block == 1 && d->M->n == n &&
                        d->M->dtype == d->dtype;
+    if (d->flags & 32) {
+        // binary16 basis storage (SolverConfig.basis_precision = "binary16")
+        if constexpr (sizeof(T) == 4) {
+            const bool ok = (!precond || diag1) && !(d->flags & 16) && !(d->flags & 4) && d->nranks <= 1 &&
+                            m + 1 <= kRegMaxCols && (uintptr_t)d->x_out % 16 == 0 && (uintptr_t)d->V % 16 == 0 &&
+                            (uintptr_t)d->work % 16 == 0 && (uintptr_t)d->r0 % 16 == 0;
+            if (!ok)
+                return fail(MPK_EUNSUPPORTED, "binary16 basis: one GPU, m <= 51, CGS2, identity or Jacobi(1)");
+            return with_op<T>(d->A, [&](auto op) -> int {
+                return launch_fused_reg<T, decltype(op), __half>(op, d, cap, tf, u, s);
+            });
+        } else {
+            return fail(MPK_EUNSUPPORTED, "binary16 basis storage needs binary32 cycles");
+        }
+    }
     if ((d->flags & 16) && (!precond || (diag1 && d->nranks <= 1)) && m + 1 <= kRegMaxCols &&
         (uintptr_t)d->x_out % 16 == 0 &&
         (uintptr_t)d->V % 16 == 0 && (uintptr_t)d->work % 16 == 0 && (uintptr_t)d->r0 % 16 == 0) {
         return with_op<T>(d->A, [&](auto op) -> int { return launch_dcgs2<T, decltype(op)>(op, d, cap, tf, u, s); });
     }
     // identity preconditioner, any m: the persistent register kernel (column
-    // blocks beyond 51 columns); MPK_FUSED_IMPL=tma keeps the TMA ring for m <= 63
-    if (!precond && !(d->flags & 4) && !fused_use_tma() && (uintptr_t)d->x_out % 16 == 0 &&
+    // blocks beyond 51 columns)
+    if (!precond && !(d->flags & 4) && (uintptr_t)d->x_out % 16 == 0 &&
         (uintptr_t)d->V % 16 == 0 && (uintptr_t)d->work % 16 == 0 && (uintptr_t)d->r0 % 16 == 0) {
         return with_op<T>(d->A, [&](auto op) -> int {
             return launch_fused_reg<T, decltype(op)>(op, d, cap, tf, u, s);
         });
     }
-    if (diag1 && m + 1 <= kRegMaxCols && !(d->flags & 4) && !fused_use_tma() &&
+    if (diag1 && m + 1 <= kRegMaxCols && !(d->flags & 4) &&
         (uintptr_t)d->x_out % 16 == 0 && (uintptr_t)d->V % 16 == 0 && (uintptr_t)d->work % 16 == 0 &&
         (uintptr_t)d->r0 % 16 == 0 && (uintptr_t)d->M->lu % 16 == 0) {
         return with_op<T>(d->A, [&](auto op) -> int {
             return launch_fused_reg<T, decltype(op)>(op, d, cap, tf, u, s);
         });
     }
-    if (!precond && m + 1 <= kFMaxCols && !(d->flags & 4)) {
-        // persistent cooperative cycle: one launch for the whole cycle
-        return with_op<T>(d->A, [&](auto op) -> int {
-            using Op = decltype(op);
-            const bool aligned = ((uintptr_t)d->x_out % 16 == 0) && ((uintptr_t)d->V % 16 == 0) &&
-                                 ((uintptr_t)d->work % 16 == 0) && ((uintptr_t)d->r0 % 16 == 0);
-            if (!fused_use_tma() && aligned && m + 1 <= kRegMaxCols) return launch_fused_reg<T, Op>(op, d, cap, tf, u, s);
-            const int tr = fused_tile_rows(sizeof(T));
-            if (tr == 256) return launch_fused<T, Op, 256>(op, d, cap, tf, u, s);
-            if (tr == 64) return launch_fused<T, Op, 64>(op, d, cap, tf, u, s);
-            return launch_fused<T, Op, 128>(op, d, cap, tf, u, s);
-        });
-    }
-
     g_last_cycle = "multi-kernel";
     k_cycle_begin<T><<<1, 32, 0, s>>>((const T *)d->rnorm2, sums, H, ctl, d->norm_scale);
     if ((rc = check_launch("k_cycle_begin"))) return rc;
@@ -1035,6 +961,29 @@ int mpk_spmv(const mpk_matrix *A, const void *x, void *y, void *stream) {
         return with_op<T>(A, [&](auto op) -> int {
             using Op = decltype(op);
             if (op.n == 0) return MPK_OK;
+            if constexpr (!Op::kStencil) {
+                const int64_t we = csr_window_elems(op, kSpmvChunk);
+                if (we > 0) {
+                    // banded rows: x window in shared memory; 16 entries per
+                    // lane when rows are long (config 5: ~49 entries)
+                    const bool wide = op.v != nullptr && A->nnz > 16 * A->n;
+                    auto kw = wide ? k_spmv_win<T, 16> : k_spmv_win<T, 8>;
+                    const size_t smem = (size_t)we * sizeof(T);
+                    // the window replaces L1 reuse: prefer shared memory so
+                    // occupancy is not capped by the default carveout
+                    static bool carve = false;
+                    if (!carve) {
+                        cudaFuncSetAttribute(k_spmv_win<T, 16>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                             (int)cudaSharedmemCarveoutMaxShared);
+                        cudaFuncSetAttribute(k_spmv_win<T, 8>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                             (int)cudaSharedmemCarveoutMaxShared);
+                        carve = true;
+                    }
+                    int g = grid_for(kw, smem, (op.n + kSpmvChunk - 1) / kSpmvChunk * kBlock);
+                    kw<<<g, kBlock, smem, s>>>(op, (const T *)x, (T *)y);
+                    return check_launch("k_spmv_win");
+                }
+            }
             auto kern = k_spmv<T, Op>;
             int g = grid_for(kern, 0, op.n);
             kern<<<g, kBlock, 0, s>>>(op, (const T *)x, (T *)y);
@@ -1208,6 +1157,27 @@ int mpk_lsq_solve(int32_t dtype, int32_t m, int32_t k, void *hess, mpk_cycle_ctl
         k_lsq_solve<float><<<1, 32, (size_t)(m + 1) * 4, s>>>(hess_view<float>(hess, m), ctl,
                                                              std::ldexp(1.0, -24), k);
     return check_launch("k_lsq_solve");
+}
+
+int mpk_block_lu(const mpk_matrix *A, int32_t k, void *lu, int32_t *piv, void *minpiv, double *thr, int32_t *bad,
+                 void *stream) {
+    if (!A || A->kind != MPK_CSR || !lu || !piv || !minpiv || !thr || !bad) return fail(MPK_EARG, "null argument");
+    if (k < 1 || k > 64) return fail(MPK_EUNSUPPORTED, "block Jacobi block size must be 1..64 on the device");
+    if (A->n == 0) return MPK_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    auto go = [&](auto tag) -> int {
+        using T = decltype(tag);
+        const CsrOp<T> op = make_csr<T>(A);
+        const double u = sizeof(T) == 8 ? 1.1102230246251565e-16 : 5.9604644775390625e-08;
+        const size_t smem = (size_t)kLuWarps * k * k * sizeof(T);
+        cudaFuncSetAttribute(k_block_lu<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const int64_t nb = (A->n + k - 1) / k;
+        int64_t g = (nb + kLuWarps - 1) / kLuWarps;
+        if (g > 8 * (int64_t)sm_count_cached()) g = 8 * (int64_t)sm_count_cached();
+        k_block_lu<T><<<(int)g, kLuWarps * 32, smem, s>>>(op, k, u, (T *)lu, piv, (T *)minpiv, thr, bad);
+        return check_launch("k_block_lu");
+    };
+    return A->dtype == MPK_F64 ? go(double{}) : go(float{});
 }
 
 int64_t mpk_launch_count(void) { return (int64_t)g_launches; }

@@ -7,8 +7,10 @@
 // and sqrt are IEEE round-to-nearest and fp32 subnormals are preserved.
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <string.h>
 
 #include "../../include/mpk_b200.h"
 
@@ -65,6 +67,71 @@ __device__ __forceinline__ void stcg16(double *p, const Pack<double> &v) {
     __stcg(reinterpret_cast<double2 *>(p), make_double2(v.v[0], v.v[1]));
 }
 
+// binary16 basis storage (SolverConfig.basis_precision = "binary16", fp32
+// cycles): 16-byte groups of 8 halves
+__device__ __forceinline__ Pack<__half> ldcg16(const __half *p) {
+    Pack<__half> r;
+    uint32_t w[4];
+    asm volatile("ld.global.cg.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                 : "l"(p));
+    memcpy(&r, w, 16);
+    return r;
+}
+
+// Basis element I/O: V stored in TV, arithmetic in T.  For TV == T the
+// value itself; binary16 stores v*s and reads back h*(1/s) with s a power of
+// two (exact scaling: it only moves the normalised basis entries, ~1/sqrt(n),
+// into binary16's normal range).
+template <typename T, typename TV> struct VIO {
+    static __device__ __forceinline__ T get(TV v, T) { return v; }
+    static __device__ __forceinline__ TV put(T v, T) { return v; }
+};
+template <> struct VIO<float, __half> {
+    static __device__ __forceinline__ float get(__half v, float si) { return __fmul_rn(__half2float(v), si); }
+    static __device__ __forceinline__ __half put(float v, float s) { return __float2half_rn(__fmul_rn(v, s)); }
+};
+
+// Raw (unscaled) values of a 16-byte basis group as T: the binary16 stream
+// kernels fold the power-of-two scale into their coefficients / partial sums
+// instead of multiplying every element (exact either way).
+template <typename T, typename TV>
+__device__ __forceinline__ void raw_vals(const Pack<TV> &p, T (&o)[16 / sizeof(TV)]) {
+    if constexpr (sizeof(TV) == sizeof(T)) {
+#pragma unroll
+        for (int e = 0; e < (int)(16 / sizeof(TV)); ++e) o[e] = p.v[e];
+    } else {
+        const __half2 *h = reinterpret_cast<const __half2 *>(p.v);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float2 f = __half22float2(h[q]);
+            o[2 * q] = f.x;
+            o[2 * q + 1] = f.y;
+        }
+    }
+}
+
+// R consecutive elements of T (16 or 32 bytes) through L2
+template <typename T, int R> __device__ __forceinline__ void ldrows(const T *p, T (&o)[R]) {
+    constexpr int E = 16 / (int)sizeof(T);
+    static_assert(R % E == 0, "whole 16-byte groups");
+#pragma unroll
+    for (int q = 0; q < R / E; ++q) {
+        const Pack<T> v = ldcg16(p + q * E);
+#pragma unroll
+        for (int e = 0; e < E; ++e) o[q * E + e] = v.v[e];
+    }
+}
+template <typename T, int R> __device__ __forceinline__ void strows(T *p, const T (&o)[R]) {
+    constexpr int E = 16 / (int)sizeof(T);
+#pragma unroll
+    for (int q = 0; q < R / E; ++q) {
+        Pack<T> v;
+#pragma unroll
+        for (int e = 0; e < E; ++e) v.v[e] = o[q * E + e];
+        stcg16(p + q * E, v);
+    }
+}
 
 // Warp-level sum (fixed butterfly order -> deterministic).
 template <typename T> __device__ __forceinline__ T warp_sum(T v) {

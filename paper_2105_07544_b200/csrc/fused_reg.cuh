@@ -27,8 +27,8 @@ namespace mpk {
 
 constexpr int kRegMaxCols = 52;          // columns per streaming block (one pass per phase when m <= 51)
 
-template <typename T> struct RegCfg {
-    static constexpr int R = 16 / (int)sizeof(T);      // rows per 16-byte group (4 fp32 / 2 fp64)
+template <typename T, typename TV = T> struct RegCfg {
+    static constexpr int R = 16 / (int)sizeof(TV);     // rows per 16-byte basis group (4 fp32 / 2 fp64 / 8 fp16)
     static constexpr int G = 8;                        // row groups per warp (128-byte fp32 / 2 x 64-byte fp64 runs)
     static constexpr int P = 32 / G;                   // column parts per warp
     static constexpr int KP = kRegMaxCols / P;         // columns per part (13)
@@ -46,13 +46,14 @@ enum { kRegDots = 0, kRegUpdateDots = 1, kRegUpdateNorm = 2, kRegCorrect = 3 };
 // U row groups per thread per trip (U * ceil(nc/P) <= KP): early in a cycle,
 // when the basis is narrow, every thread still keeps ~KP 16-byte loads in
 // flight instead of paying one memory latency per 32 rows.
-template <typename T, int MODE, int U>
-__device__ __forceinline__ void reg_phase_u(const T *V, int64_t ld, int nc, int64_t rb, int64_t re, int64_t n,
+template <typename T, typename TV, int MODE, int U, int KU>
+__device__ __forceinline__ void reg_phase_u(const TV *V, int64_t ld, int nc, int64_t rb, int64_t re, int64_t n,
                                             const T *x, T *y, const T *coef, T (&acc)[RegCfg<T>::KP], T &ext,
-                                            const CommArgs<T> *cm, const T *diag, bool rev) {
-    using C = RegCfg<T>;
+                                            const CommArgs<T> *cm, const T *diag, bool rev, T vsi) {
+    using C = RegCfg<T, TV>;
     constexpr int R = C::R;
-    constexpr int KU = C::KP / U;             // columns per part held per row group
+    constexpr bool half = sizeof(TV) != sizeof(T);
+    static_assert(KU <= C::KP, "columns per part");   // KU: columns per part held per row group
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane % C::G, p = lane / C::G;
     constexpr int64_t TRIP = (int64_t)C::WR * U;
@@ -63,8 +64,8 @@ __device__ __forceinline__ void reg_phase_u(const T *V, int64_t ld, int nc, int6
     const int64_t ntrip = (b0 < re) ? (re - b0 + step - 1) / step : 0;
     for (int64_t t = 0; t < ntrip; ++t) {
         const int64_t b = b0 + (rev ? ntrip - 1 - t : t) * step;
-        Pack<T> vv[U][KU];
-        Pack<T> xv[U];
+        Pack<TV> vv[U][KU];
+        T xv[U][R];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int64_t r = b + (int64_t)(u * C::G + g) * R;
@@ -75,21 +76,21 @@ __device__ __forceinline__ void reg_phase_u(const T *V, int64_t ld, int nc, int6
                 if (c < nc && live) vv[u][i] = ldcg16(V + (int64_t)c * ld + r);
                 else {
 #pragma unroll
-                    for (int e = 0; e < R; ++e) vv[u][i].v[e] = T(0);
+                    for (int e = 0; e < R; ++e) vv[u][i].v[e] = TV(0.0f);
                 }
             }
             if (MODE == kRegCorrect) {
 #pragma unroll
                 for (int e = 0; e < R; ++e)
-                    xv[u].v[e] = (p == 0 && live && r + e < n) ? x[r + e] : T(0);   // x may alias y
+                    xv[u][e] = (p == 0 && live && r + e < n) ? x[r + e] : T(0);   // x may alias y
             } else if (MODE == kRegUpdateNorm && p != 0) {
 #pragma unroll
-                for (int e = 0; e < R; ++e) xv[u].v[e] = T(0);   // only part 0 uses x (x may alias y)
+                for (int e = 0; e < R; ++e) xv[u][e] = T(0);   // only part 0 uses x (x may alias y)
             } else if (live) {
-                xv[u] = ldcg16(x + r);
+                ldrows<T, R>(x + r, xv[u]);
             } else {
 #pragma unroll
-                for (int e = 0; e < R; ++e) xv[u].v[e] = T(0);
+                for (int e = 0; e < R; ++e) xv[u][e] = T(0);
             }
         }
 #pragma unroll
@@ -100,8 +101,10 @@ __device__ __forceinline__ void reg_phase_u(const T *V, int64_t ld, int nc, int6
 #pragma unroll
                 for (int i = 0; i < KU; ++i) {
                     if (p + C::P * i < nc) {
+                        T vr[R];
+                        raw_vals<T, TV>(vv[u][i], vr);
 #pragma unroll
-                        for (int e = 0; e < R; ++e) acc[i] += vv[u][i].v[e] * xv[u].v[e];
+                        for (int e = 0; e < R; ++e) acc[i] += vr[e] * xv[u][e];
                     }
                 }
                 continue;
@@ -113,9 +116,13 @@ __device__ __forceinline__ void reg_phase_u(const T *V, int64_t ld, int nc, int6
             for (int i = 0; i < KU; ++i) {
                 const int c = p + C::P * i;
                 if (c < nc) {
-                    const T cf = coef[c];
+                    // binary16: the stored values carry the scale vs, folded
+                    // into the coefficient (vsi is a power of two: exact)
+                    const T cf = half ? coef[c] * vsi : coef[c];
+                    T vr[R];
+                    raw_vals<T, TV>(vv[u][i], vr);
 #pragma unroll
-                    for (int e = 0; e < R; ++e) s[e] += vv[u][i].v[e] * cf;
+                    for (int e = 0; e < R; ++e) s[e] += vr[e] * cf;
                 }
             }
 #pragma unroll
@@ -129,52 +136,77 @@ __device__ __forceinline__ void reg_phase_u(const T *V, int64_t ld, int nc, int6
                 for (int e = 0; e < R; ++e)
                     if (r + e < n) s[e] = RN<T>::div(s[e], __ldg(diag + r + e));
             }
-            Pack<T> yv;
+            T yv[R];
 #pragma unroll
             for (int e = 0; e < R; ++e)
-                yv.v[e] = (MODE == kRegCorrect) ? RN<T>::add(xv[u].v[e], s[e]) : RN<T>::sub(xv[u].v[e], s[e]);
+                yv[e] = (MODE == kRegCorrect) ? RN<T>::add(xv[u][e], s[e]) : RN<T>::sub(xv[u][e], s[e]);
             if (p == 0 && live) {
                 if (MODE == kRegCorrect && r + R > n) {
 #pragma unroll
                     for (int e = 0; e < R; ++e)
-                        if (r + e < n) y[r + e] = yv.v[e];
+                        if (r + e < n) y[r + e] = yv[e];
                 } else {
-                    stcg16(y + r, yv);
+                    strows<T, R>(y + r, yv);
                 }
                 if (MODE == kRegUpdateNorm && cm != nullptr) {
                     // halo rows of w'' for the other ranks' next SpMV (P2P)
                     for (int q = 0; q < cm->nranks; ++q)
                         if (q != cm->rank && r >= cm->mir_lo[q] && r < cm->mir_hi[q])
-                            stcg16(cm->xg[q] + cm->row0 + r, yv);
+                            strows<T, R>(cm->xg[q] + cm->row0 + r, yv);
                 }
             }
             if (MODE == kRegUpdateDots) {
 #pragma unroll
                 for (int i = 0; i < KU; ++i) {
                     if (p + C::P * i < nc) {
+                        T vr[R];
+                        raw_vals<T, TV>(vv[u][i], vr);
 #pragma unroll
-                        for (int e = 0; e < R; ++e) acc[i] += vv[u][i].v[e] * yv.v[e];
+                        for (int e = 0; e < R; ++e) acc[i] += vr[e] * yv[e];
                     }
                 }
             }
             if (MODE == kRegUpdateNorm && p == 0) {
 #pragma unroll
-                for (int e = 0; e < R; ++e) ext += yv.v[e] * yv.v[e];
+                for (int e = 0; e < R; ++e) ext += yv[e] * yv[e];
             }
         }
     }
+    if constexpr (half) {
+        // dots against the stored (scaled) basis: undo the scale once
+#pragma unroll
+        for (int i = 0; i < KU; ++i) acc[i] *= vsi;
+    }
 }
 
-template <typename T, int MODE>
-__device__ __forceinline__ void reg_phase(const T *V, int64_t ld, int nc, int64_t rb, int64_t re, int64_t n,
+template <typename T, int MODE, typename TV = T>
+__device__ __forceinline__ void reg_phase(const TV *V, int64_t ld, int nc, int64_t rb, int64_t re, int64_t n,
                                           const T *x, T *y, const T *coef, T (&acc)[RegCfg<T>::KP], T &ext,
-                                          const CommArgs<T> *cm = nullptr, const T *diag = nullptr, bool rev = false) {
-    using C = RegCfg<T>;
+                                          const CommArgs<T> *cm = nullptr, const T *diag = nullptr, bool rev = false,
+                                          T vsi = T(1)) {
+    using C = RegCfg<T, TV>;
     const int ncp = (nc + C::P - 1) / C::P;   // columns per part
-    if (ncp * 8 <= C::KP) reg_phase_u<T, MODE, 8>(V, ld, nc, rb, re, n, x, y, coef, acc, ext, cm, diag, rev);
-    else if (ncp * 4 <= C::KP) reg_phase_u<T, MODE, 4>(V, ld, nc, rb, re, n, x, y, coef, acc, ext, cm, diag, rev);
-    else if (ncp * 2 <= C::KP) reg_phase_u<T, MODE, 2>(V, ld, nc, rb, re, n, x, y, coef, acc, ext, cm, diag, rev);
-    else reg_phase_u<T, MODE, 1>(V, ld, nc, rb, re, n, x, y, coef, acc, ext, cm, diag, rev);
+    // (U row groups, KU columns) per thread and trip: 12-18 sixteen-byte
+    // loads in flight at every basis width.  Measured on B200 (phase-B pass,
+    // tools/micro/stream_b_sweep.cu): the exact-width (2, 7..9) and (3, 4)
+    // shapes stream 6.4-7.1 TB/s where (1, 13) with 7-9 live columns gave
+    // 5.2-5.9 and (2, 6) with 4 gave 6.1-6.6; (2, 10..11) spill.
+#define MPK_REG_U(UU, KK) \
+    reg_phase_u<T, TV, MODE, UU, KK>(V, ld, nc, rb, re, n, x, y, coef, acc, ext, cm, diag, rev, vsi)
+    static_assert(C::KP == 13, "shape table below assumes 13 columns per part");
+    switch (ncp) {
+        case 1: MPK_REG_U(8, 1); break;
+        case 2:
+        case 3: MPK_REG_U(4, 3); break;
+        case 4: MPK_REG_U(3, 4); break;
+        case 5:
+        case 6: MPK_REG_U(2, 6); break;
+        case 7: MPK_REG_U(2, 7); break;
+        case 8: MPK_REG_U(2, 8); break;
+        case 9: MPK_REG_U(2, 9); break;
+        default: MPK_REG_U(1, 13); break;
+    }
+#undef MPK_REG_U
 }
 
 // CTA partials of the register layout: column c lives in part p = c % P,
@@ -223,10 +255,28 @@ __device__ __forceinline__ void reg_write_partials(T (&acc)[RegCfg<T>::KP], int 
 // ||w||^2.  Out of line (noinline) so its register needs (BentPipe
 // coefficient arithmetic, the CSR staging) do not raise register pressure in
 // the streaming phases, which are kept spill-free.
-template <typename T, class Op>
-__device__ __noinline__ T phase_a_spmv(const Op &A, const XSlab<T> xs, T *w, int64_t rb, int64_t re, T *sstage) {
+constexpr int kRegCsrChunk = 1024;   // rows per x-window chunk of a banded CSR SpMV (phase A)
+
+template <typename T, class Op, class XS>
+__device__ __noinline__ T phase_a_spmv(const Op &A, const XS xs, T *w, int64_t rb, int64_t re, T *sstage,
+                                       T *swin) {
     T an = T(0);
     if constexpr (!Op::kStencil) {
+        if (swin != nullptr) {
+            // banded rows: x of each 1024-row chunk (+- band) staged in shared memory
+            T *sb = sstage + (threadIdx.x >> 5) * kCsrWarpBuf;
+            const bool wide = sizeof(T) == 4 && A.rp[A.n] > 16 * (int64_t)A.n;
+            for (int64_t R = rb; R < re; R += kRegCsrChunk) {
+                const int64_t Re = R + kRegCsrChunk < re ? R + kRegCsrChunk : re;
+                auto put = [&](int64_t r, T wr) {
+                    w[r] = wr;
+                    an += wr * wr;
+                };
+                if (wide) csr_chunk<16>(A, xs, R, Re, swin, sb, put);
+                else csr_chunk<8>(A, xs, R, Re, swin, sb, put);
+            }
+            return an;
+        }
         // CSR: warp-cooperative 32-row groups (coalesced entries, row-sequential sums)
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         T *sb = sstage + warp * kCsrWarpBuf;
@@ -241,11 +291,28 @@ __device__ __noinline__ T phase_a_spmv(const Op &A, const XSlab<T> xs, T *w, int
         }
     } else if (A.group_ok()) {
         // 16-byte row groups: vector reads of the group and its S/N (B/U)
-        // neighbours, one group per thread per trip
+        // neighbours; UG groups per thread per trip with every group's loads
+        // issued before any is evaluated (||w||^2 summed in row order as
+        // with one group per trip)
         constexpr int R = RegCfg<T>::R;
+        constexpr int UG = 4;
         auto xv = [&](int64_t c) { return xs.vec(c); };
         constexpr int64_t S = (int64_t)kFB * R;
-        for (int64_t r = rb + (int64_t)threadIdx.x * R; r < re; r += S) {
+        int64_t r = rb + (int64_t)threadIdx.x * R;
+        for (; r + (UG - 1) * S < re; r += UG * S) {
+            typename Op::GroupIn in[UG];
+#pragma unroll
+            for (int u = 0; u < UG; ++u) A.group_load(r + u * S, xv, xs, in[u]);
+#pragma unroll
+            for (int u = 0; u < UG; ++u) {
+                Pack<T> o;
+                A.group_eval(r + u * S, in[u], o.v);
+                stcg16(w + r + u * S, o);
+#pragma unroll
+                for (int e = 0; e < R; ++e) an += o.v[e] * o.v[e];
+            }
+        }
+        for (; r < re; r += S) {
             Pack<T> o;
             A.row_group(r, xv, xs, o.v);
             stcg16(w + r, o);
@@ -275,9 +342,13 @@ __device__ __noinline__ T phase_a_spmv(const Op &A, const XSlab<T> xs, T *w, int
     return an;
 }
 
-template <typename T, class Op, bool BIG, bool MULTI>
+template <typename T, class Op, bool BIG, bool MULTI, typename TV = T>
 __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
     using C = RegCfg<T>;
+    using IO = VIO<T, TV>;
+    // basis storage: T, or binary16 holding v * vs (fp32 cycles, one GPU, m <= 51)
+    TV *const Vb = reinterpret_cast<TV *>(a.V);
+    const T vs = a.vs, vsi = a.vsi;
     extern __shared__ __align__(16) unsigned char dsm_reg[];
     const int m = a.m, ldr = m + 1;
     // big (m + 1 > 52 columns): the basis is streamed in blocks of 52 columns
@@ -295,6 +366,7 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
     T *sred = sc2 + nslot;                     // kFW * kFSlots
     T *sctmp = sred + kFW * kFSlots;           // big: nslot (the column being rotated)
     T *sstage = sctmp + (big ? nslot : 0);     // kFW * kCsrWarpBuf (CSR SpMV staging)
+    T *swin = a.csr_win ? sstage + kFW * kCsrWarpBuf : nullptr;   // banded CSR x window
     const int xslot = big ? m + 1 : kFExtra;   // partial slot of the extra scalar
     __shared__ T s_gamma, s_beta, s_bn2;
     __shared__ int s_done, s_steps, s_break, s_app;
@@ -387,7 +459,7 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
         MPK_MARK(12);
         const T *src = (k == 0 && !multi) ? a.r0 : a.wpp;
         const T dv = (k == 0) ? s_gamma : s_beta;
-        T *vk = a.V + (int64_t)k * a.ld;
+        TV *vk = Vb + (int64_t)k * a.ld;
         T acc[C::KP];
         T ext = T(0);
         // ---------------- phase A: v_k = src/dv, w = A v_k, ||w||^2 ; c1 = V^T w
@@ -406,7 +478,9 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
                 for (int u = 0; u < 4; ++u) {
 #pragma unroll
                     for (int e = 0; e < R; ++e) q[u].v[e] = RN<T>::div(q[u].v[e], dv);
-                    stcg16(vk + r + u * S, q[u]);
+                    stv<T, TV>(vk + r + u * S, q[u], vs);
+#pragma unroll
+                    for (int e = 0; e < R; ++e) q[u].v[e] = IO::get(IO::put(q[u].v[e], vs), vsi);   // as stored
                     if (a.diag) {
 #pragma unroll
                         for (int e = 0; e < R; ++e) q[u].v[e] = RN<T>::div(q[u].v[e], __ldg(a.diag + r + u * S + e));
@@ -418,7 +492,9 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
                 Pack<T> q = ldcg16(src + r);
 #pragma unroll
                 for (int e = 0; e < R; ++e) q.v[e] = RN<T>::div(q.v[e], dv);
-                stcg16(vk + r, q);
+                stv<T, TV>(vk + r, q, vs);
+#pragma unroll
+                for (int e = 0; e < R; ++e) q.v[e] = IO::get(IO::put(q.v[e], vs), vsi);
                 if (a.diag) {
 #pragma unroll
                     for (int e = 0; e < R; ++e) q.v[e] = RN<T>::div(q.v[e], __ldg(a.diag + r + e));
@@ -426,14 +502,15 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
                 }
             }
             for (int64_t t = rv + tid; t < re; t += kFB) {
-                const T v = RN<T>::div(__ldcg(src + t), dv);
-                vk[t] = v;
+                const TV hv = IO::put(RN<T>::div(__ldcg(src + t), dv), vs);
+                vk[t] = hv;
+                const T v = IO::get(hv, vsi);
                 if (a.diag) a.z[t] = RN<T>::div(v, __ldg(a.diag + t));
             }
         }
         MPK_MARK(0);
         __syncthreads();
-        an = phase_a_spmv<T>(A, XSlab<T>{src, vk, dv, rb, re, a.diag, a.z}, a.w, rb, re, sstage);
+        an = phase_a_spmv<T>(A, XSlab<T, TV>{src, vk, dv, rb, re, a.diag, a.z, vs, vsi}, a.w, rb, re, sstage, swin);
         MPK_MARK(1);
         __syncthreads();   // w rows of this CTA visible to the other lanes' 16-byte loads
         const int nbk = BIG ? (nc + kRegMaxCols - 1) / kRegMaxCols : 1;   // column blocks
@@ -444,8 +521,8 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
         if (!BIG) {
 #pragma unroll
             for (int i = 0; i < C::KP; ++i) acc[i] = T(0);
-            reg_phase<T, kRegDots>(a.V, a.ld, nc, rb, re, a.n, a.w, nullptr, nullptr, acc, ext, nullptr, nullptr,
-                                   (3 * k) & 1);
+            reg_phase<T, kRegDots, TV>(Vb, a.ld, nc, rb, re, a.n, a.w, nullptr, nullptr, acc, ext, nullptr, nullptr,
+                                   (3 * k) & 1, vsi);
             MPK_MARK(2);
             reg_write_partials<T>(acc, nc, an, sred, partA, cmp, 0, 0, true, xslot);
         } else {
@@ -454,7 +531,7 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
                 blk(bi, nc, c0, cn);
 #pragma unroll
                 for (int i = 0; i < C::KP; ++i) acc[i] = T(0);
-                reg_phase<T, kRegDots>(a.V + (int64_t)c0 * a.ld, a.ld, cn, rb, re, a.n, a.w, nullptr, nullptr, acc,
+                reg_phase<T, kRegDots, TV>(Vb + (int64_t)c0 * a.ld, a.ld, cn, rb, re, a.n, a.w, nullptr, nullptr, acc,
                                        ext);
                 reg_write_partials<T>(acc, cn, an, sred, partA, nullptr, 0, c0, bi == nbk - 1, xslot);
             }
@@ -469,8 +546,8 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
         if (!BIG) {
 #pragma unroll
             for (int i = 0; i < C::KP; ++i) acc[i] = T(0);
-            reg_phase<T, kRegUpdateDots>(a.V, a.ld, nc, rb, re, a.n, a.w, a.wp, sc1, acc, ext, nullptr, nullptr,
-                                         (3 * k + 1) & 1);
+            reg_phase<T, kRegUpdateDots, TV>(Vb, a.ld, nc, rb, re, a.n, a.w, a.wp, sc1, acc, ext, nullptr, nullptr,
+                                         (3 * k + 1) & 1, vsi);
             MPK_MARK(5);
             reg_write_partials<T>(acc, nc, T(0), sred, partB, cmp, pblk, 0, true, xslot);
         } else {
@@ -480,7 +557,7 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
                 int c0, cn;
                 blk(bi, nc, c0, cn);
                 T dummy = T(0);
-                reg_phase<T, kRegUpdateNorm>(a.V + (int64_t)c0 * a.ld, a.ld, cn, rb, re, a.n, bi ? a.wp : a.w, a.wp,
+                reg_phase<T, kRegUpdateNorm, TV>(Vb + (int64_t)c0 * a.ld, a.ld, cn, rb, re, a.n, bi ? a.wp : a.w, a.wp,
                                              sc1 + c0, acc, dummy);
                 __syncthreads();
             }
@@ -489,7 +566,7 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
                 blk(bi, nc, c0, cn);
 #pragma unroll
                 for (int i = 0; i < C::KP; ++i) acc[i] = T(0);
-                reg_phase<T, kRegDots>(a.V + (int64_t)c0 * a.ld, a.ld, cn, rb, re, a.n, a.wp, nullptr, nullptr, acc,
+                reg_phase<T, kRegDots, TV>(Vb + (int64_t)c0 * a.ld, a.ld, cn, rb, re, a.n, a.wp, nullptr, nullptr, acc,
                                        ext);
                 reg_write_partials<T>(acc, cn, T(0), sred, partB, nullptr, pblk, c0, false, xslot);
             }
@@ -503,14 +580,14 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
         // ---------------- phase C: w'' = w' - V c2 ; ||w''||^2
         T bn = T(0);
         if (!BIG) {
-            reg_phase<T, kRegUpdateNorm>(a.V, a.ld, nc, rb, re, a.n, a.wp, a.wpp, sc2, acc, bn, cmp, nullptr,
-                                         (3 * k + 2) & 1);
+            reg_phase<T, kRegUpdateNorm, TV>(Vb, a.ld, nc, rb, re, a.n, a.wp, a.wpp, sc2, acc, bn, cmp, nullptr,
+                                         (3 * k + 2) & 1, vsi);
         } else {
             for (int bi = 0; bi < nbk; ++bi) {
                 int c0, cn;
                 blk(bi, nc, c0, cn);
                 T dummy = T(0);
-                reg_phase<T, kRegUpdateNorm>(a.V + (int64_t)c0 * a.ld, a.ld, cn, rb, re, a.n, bi ? a.wpp : a.wp,
+                reg_phase<T, kRegUpdateNorm, TV>(Vb + (int64_t)c0 * a.ld, a.ld, cn, rb, re, a.n, bi ? a.wpp : a.wp,
                                              a.wpp, sc2 + c0, acc, bi == nbk - 1 ? bn : dummy);
                 __syncthreads();
             }
@@ -553,8 +630,8 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
         for (int i = tid; i <= k; i += kFB) a.H.g[i] = sg[i];
     }
     if (a.final_col && k > 0 && !s_break) {
-        T *vn = a.V + (int64_t)k * a.ld;
-        for (int64_t r = rb + tid; r < re; r += kFB) vn[r] = RN<T>::div(a.wpp[r], s_beta);
+        TV *vn = Vb + (int64_t)k * a.ld;
+        for (int64_t r = rb + tid; r < re; r += kFB) vn[r] = IO::put(RN<T>::div(a.wpp[r], s_beta), vs);
     }
     if (k == 0) {
         for (int64_t r = rb + tid; r < re; r += kFB) a.x_out[r] = a.x0[r];
@@ -564,12 +641,12 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
         T acc[C::KP];
         T ext = T(0);
         if (!BIG) {
-            reg_phase<T, kRegCorrect>(a.V, a.ld, k, rb, re, a.n, a.x0, a.x_out, sd, acc, ext, nullptr, a.diag,
-                                      (3 * k) & 1);   // after step k-1's phase C (index 3k-1)
+            reg_phase<T, kRegCorrect, TV>(Vb, a.ld, k, rb, re, a.n, a.x0, a.x_out, sd, acc, ext, nullptr, a.diag,
+                                      (3 * k) & 1, vsi);   // after step k-1's phase C (index 3k-1)
         } else {   // big: x += V_b d_b block by block (no diagonal preconditioner here)
             for (int c0 = 0; c0 < k; c0 += kRegMaxCols) {
                 const int cn = (k - c0 < kRegMaxCols) ? k - c0 : kRegMaxCols;
-                reg_phase<T, kRegCorrect>(a.V + (int64_t)c0 * a.ld, a.ld, cn, rb, re, a.n, c0 ? a.x_out : a.x0,
+                reg_phase<T, kRegCorrect, TV>(Vb + (int64_t)c0 * a.ld, a.ld, cn, rb, re, a.n, c0 ? a.x_out : a.x0,
                                           a.x_out, sd + c0, acc, ext);
                 __syncthreads();
             }

@@ -64,7 +64,23 @@ __device__ __forceinline__ void for_rows(const Op &A, X x, T *sb, F &&fn) {
             // neighbours), bit-identical to row(); scalar tail past n - n % R
             const int64_t ng = A.n / R;
             auto xv = [&](int64_t c) { return x.vec(c); };
-            for (int64_t gi = gtid(); gi < ng; gi += gstride()) {
+            // two groups per thread per trip, both groups' loads in flight
+            // before either is evaluated (fn still sees rows in stride order)
+            const int64_t st = gstride();
+            int64_t gi = gtid();
+            for (; gi + st < ng; gi += 2 * st) {
+                typename Op::GroupIn in0, in1;
+                A.group_load(gi * R, xv, x, in0);
+                A.group_load((gi + st) * R, xv, x, in1);
+                T o[R];
+                A.group_eval(gi * R, in0, o);
+#pragma unroll
+                for (int e = 0; e < R; ++e) fn(gi * R + e, o[e]);
+                A.group_eval((gi + st) * R, in1, o);
+#pragma unroll
+                for (int e = 0; e < R; ++e) fn((gi + st) * R + e, o[e]);
+            }
+            for (; gi < ng; gi += st) {
                 T o[R];
                 A.row_group(gi * R, xv, x, o);
 #pragma unroll
@@ -519,6 +535,21 @@ __global__ void __launch_bounds__(kBlock) k_spmv(Op A, const T *__restrict__ x, 
     for_rows<T>(A, XPlain<T>{x}, sb, [&](int64_t r, T yr) { y[r] = yr; });
 }
 
+// Banded CSR (A.band > 0): chunks of kSpmvChunk rows per CTA, x staged in a
+// shared-memory window per chunk (csr_chunk), K entries per lane in flight.
+constexpr int kSpmvChunk = 1024;
+template <typename T, int K>
+__global__ void __launch_bounds__(kBlock) k_spmv_win(CsrOp<T> A, const T *__restrict__ x, T *__restrict__ y) {
+    extern __shared__ __align__(16) unsigned char dsm_win[];
+    __shared__ T sbuf[(kBlock / 32) * kCsrWarpBuf];
+    T *sx = reinterpret_cast<T *>(dsm_win);
+    T *sb = sbuf + (threadIdx.x >> 5) * kCsrWarpBuf;
+    for (int64_t R = (int64_t)blockIdx.x * kSpmvChunk; R < A.n; R += (int64_t)gridDim.x * kSpmvChunk) {
+        const int64_t Re = R + kSpmvChunk < A.n ? R + kSpmvChunk : A.n;
+        csr_chunk<K>(A, XPlain<T>{x}, R, Re, sx, sb, [&](int64_t r, T yr) { y[r] = yr; });
+    }
+}
+
 template <typename S, typename D>
 __global__ void k_convert(int64_t n, const S *__restrict__ s, D *__restrict__ d) {
     for (int64_t i = gtid(); i < n; i += gstride()) {
@@ -610,6 +641,130 @@ __global__ void k_jacobi(int64_t n, int k, const T *__restrict__ lu, const int32
             xb[i] = RN<T>::div(a, L[i * k + i]);
         }
         for (int i = 0; i < kb; ++i) out[s + i] = xb[i];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Block-Jacobi setup on the device (preconditioners.py:96-130): dense k x k
+// diagonal blocks of a CSR matrix, LU with partial pivoting, pivot test.
+// ---------------------------------------------------------------------------
+// numpy's pairwise sum of n contiguous |a_i| (np.abs(block).sum(axis=1) of
+// the reference's threshold, preconditioners.py:120): 8 strided
+// accumulators for n >= 8, combined ((0+1)+(2+3))+((4+5)+(6+7)), then the
+// remainder; sequential from -0.0 below 8 (checked bit-exact against numpy).
+template <typename T> __device__ T np_abs_pairwise(const T *a, int n) {
+    if (n < 8) {
+        T r = T(-0.0);
+        for (int i = 0; i < n; ++i) r = RN<T>::add(r, fabs(a[i]));
+        return r;
+    }
+    T r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = fabs(a[j]);
+    int i = 8;
+    for (; i < n - (n % 8); i += 8)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = RN<T>::add(r[j], fabs(a[i + j]));
+    T res = RN<T>::add(RN<T>::add(RN<T>::add(r[0], r[1]), RN<T>::add(r[2], r[3])),
+                       RN<T>::add(RN<T>::add(r[4], r[5]), RN<T>::add(r[6], r[7])));
+    for (; i < n; ++i) res = RN<T>::add(res, fabs(a[i]));
+    return res;
+}
+
+// One warp per block b (rows/columns [b*k, b*k + kb)), the block in shared
+// memory (kb x kb, row-major).  Right-looking LU with partial pivoting in T:
+// pivot = first row of maximal |a_ij| (LAPACK i?amax), full-row swap, the
+// column below scaled by the reciprocal pivot (getf2 for |pivot| >= the
+// smallest normal, division otherwise), rank-1 update of the trailing block.
+// Output in the apply kernel's layout: lu[b][i][j] (stride k), piv[b*k + i]
+// 0-based (scipy lu_factor).  minpiv[b] = min |u_ii|, thr[b] =
+// (kb*u)*max row sum (double, as the reference's Python arithmetic);
+// *bad = lowest failing block (atomicMin; the caller initialises INT32_MAX).
+// The factors agree with LAPACK's to rounding, not bit for bit (OpenBLAS
+// getrf is left-looking/recursive with FMA kernels).
+constexpr int kLuWarps = 4;
+template <typename T>
+__global__ void __launch_bounds__(kLuWarps * 32) k_block_lu(CsrOp<T> A, int k, double u, T *__restrict__ lu,
+                                                           int32_t *__restrict__ piv, T *__restrict__ minpiv,
+                                                           double *__restrict__ thr, int32_t *bad) {
+    extern __shared__ __align__(16) unsigned char dsm_lu[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    T *S = reinterpret_cast<T *>(dsm_lu) + (size_t)wib * k * k;
+    const int64_t nb = (A.n + k - 1) / k;
+    const T tiny = sizeof(T) == 8 ? T(2.2250738585072014e-308) : T(1.17549435e-38f);
+    for (int64_t b = (int64_t)blockIdx.x * kLuWarps + wib; b < nb; b += (int64_t)gridDim.x * kLuWarps) {
+        const int64_t s = b * k;
+        const int kb = (int)(A.n - s < k ? A.n - s : k);
+        for (int i = lane; i < kb * kb; i += 32) S[i] = T(0);
+        __syncwarp();
+        for (int i = lane; i < kb; i += 32) {
+            const int32_t p0 = A.rp[s + i], p1 = A.rp[s + i + 1];
+            for (int32_t p = p0; p < p1; ++p) {
+                const int64_t c = A.ci[p];
+                if (c >= s && c < s + kb) S[i * kb + (int)(c - s)] = A.v[p];
+            }
+        }
+        __syncwarp();
+        T rmax = T(0);
+        for (int i = lane; i < kb; i += 32) rmax = fmax(rmax, np_abs_pairwise(S + i * kb, kb));
+        for (int o = 16; o; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+        const double th = __dmul_rn(__dmul_rn((double)kb, u), (double)rmax);
+        for (int j = 0; j < kb; ++j) {
+            T best = T(-1);
+            int bi = kb;
+            for (int i = j + lane; i < kb; i += 32) {
+                const T a = fabs(S[i * kb + j]);
+                if (a > best) {
+                    best = a;
+                    bi = i;
+                }
+            }
+            for (int o = 16; o; o >>= 1) {
+                const T ob = __shfl_xor_sync(0xffffffffu, best, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (ob > best || (ob == best && oi < bi)) {
+                    best = ob;
+                    bi = oi;
+                }
+            }
+            const int p = bi < kb ? bi : j;
+            if (lane == 0) piv[b * k + j] = p;
+            if (p != j)
+                for (int l = lane; l < kb; l += 32) {
+                    const T t = S[j * kb + l];
+                    S[j * kb + l] = S[p * kb + l];
+                    S[p * kb + l] = t;
+                }
+            __syncwarp();
+            const T d = S[j * kb + j];
+            if (d != T(0)) {
+                const bool recip = fabs(d) >= tiny;
+                const T r = RN<T>::div(T(1), d);
+                for (int i = j + 1 + lane; i < kb; i += 32)
+                    S[i * kb + j] = recip ? RN<T>::mul(S[i * kb + j], r) : RN<T>::div(S[i * kb + j], d);
+            }
+            __syncwarp();
+            for (int i = j + 1 + lane; i < kb; i += 32) {
+                const T lij = S[i * kb + j];
+                for (int l = j + 1; l < kb; ++l) S[i * kb + l] = fma(-lij, S[j * kb + l], S[i * kb + l]);
+            }
+            __syncwarp();
+        }
+        T mp = T(INFINITY);
+        for (int i = lane; i < kb; i += 32) mp = fmin(mp, fabs(S[i * kb + i]));
+        for (int o = 16; o; o >>= 1) mp = fmin(mp, __shfl_xor_sync(0xffffffffu, mp, o));
+        T *L = lu + (size_t)b * k * k;
+        for (int e = lane; e < k * k; e += 32) {
+            const int i = e / k, l = e % k;
+            L[e] = (i < kb && l < kb) ? S[i * kb + l] : T(0);
+        }
+        for (int i = kb + lane; i < k; i += 32) piv[b * k + i] = i;
+        if (lane == 0) {
+            minpiv[b] = mp;
+            thr[b] = th;
+            if (!((double)mp > th)) atomicMin(bad, (int32_t)b);
+        }
+        __syncwarp();
     }
 }
 

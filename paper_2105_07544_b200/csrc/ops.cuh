@@ -26,6 +26,13 @@ template <typename T> struct CsrOp {
     const int32_t *__restrict__ rp;
     const int32_t *__restrict__ ci;
     const T *__restrict__ v;
+    // x-window half-width (0: off).  Banded matrices (90-99%
+    // of the columns within +-2000 of the row) gather x from a shared-memory
+    // copy of x[R - band, R + T + band) for a chunk of T rows (csr_chunk);
+    // the global gathers of irregular rows otherwise saturate L1 (one
+    // wavefront per entry: C5 ran at 90% L1/TEX throughput, 28% DRAM).
+    int64_t band = 0;
+    int64_t nnz_ = 0;    // stored entries (row statistics for the window choice)
 
     template <class X> __device__ __forceinline__ T row(int64_t r, X x) const {
         const int32_t p0 = __ldg(rp + r), p1 = __ldg(rp + r + 1);
@@ -97,6 +104,36 @@ template <typename T> struct CsrOp {
     }
     static constexpr bool kStencil = false;
 };
+
+// x accessor of a chunk: columns inside [lo, hi) from the shared-memory
+// window, the rest (far columns) through the wrapped accessor.  Same values,
+// so the row sums stay bit-identical.
+template <typename T, class X> struct XWin {
+    X x;
+    const T *sx;
+    int64_t lo, hi;
+    __device__ __forceinline__ T operator()(int64_t c) const { return (c >= lo && c < hi) ? sx[c - lo] : x(c); }
+};
+
+// Rows [R, Re) of a CSR operator by the whole CTA: x[lo, hi) (lo = R - band,
+// hi = Re + band, clipped to [0, n)) is staged in `sx` (coalesced), then the
+// warps evaluate 32-row groups with warp_rows<K> reading x through the
+// window; fn(r, y_r) runs on the lane owning row r.  All threads of the CTA
+// must call it (two __syncthreads).
+template <int K, typename T, class X, class F>
+__device__ __forceinline__ void csr_chunk(const CsrOp<T> &A, X x, int64_t R, int64_t Re, T *sx, T *sb, F &&fn) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int64_t lo = R - A.band > 0 ? R - A.band : 0;
+    const int64_t hi = Re + A.band < A.n ? Re + A.band : A.n;
+    __syncthreads();   // the previous chunk's readers are done with sx
+    for (int64_t c = lo + threadIdx.x; c < hi; c += blockDim.x) sx[c - lo] = x(c);
+    __syncthreads();
+    const XWin<T, X> xw{x, sx, lo, hi};
+    for (int64_t r0 = R + (int64_t)warp * 32; r0 < Re; r0 += (int64_t)nw * 32) {
+        const T y = A.template warp_rows<K>(r0, Re, xw, sb);
+        if (r0 + lane < Re) fn(r0 + lane, y);
+    }
+}
 
 // Division by a grid-invariant divisor (nx, nx^2) without the integer
 // divider: q = (umulhi(x, mul) + x) >> shift, exact for x < 2^31.
@@ -191,45 +228,64 @@ template <typename T> struct StencilOp {
     __device__ __forceinline__ bool group_ok() const {
         return k.preset != MPK_STRETCHED2D && k.nx % R == 0 && k.row0 % R == 0;
     }
+    // Inputs of one row group (group_load), so callers can issue several
+    // groups' loads before evaluating any (group_eval): the neighbour packs
+    // a group needs (pb/pu: Laplace3D only) and the W/E end values.
+    struct GroupIn {
+        Pack<T> c, pb, ps, pn, pu;
+        T xw, xe;
+    };
     template <class XV, class XS>
-    __device__ __forceinline__ void row_group(int64_t r, XV xv, XS xs, T (&out)[R]) const {
+    __device__ __forceinline__ void group_load(int64_t r, XV xv, XS xs, GroupIn &in) const {
         const uint32_t g = (uint32_t)(k.row0 + r);
         const int nx = k.nx;
         const uint32_t q1 = k.dnx.div(g);
         const int ix0 = (int)(g - q1 * (uint32_t)nx);
-        const Pack<T> c = xv(r);
-        const T xw = (ix0 > 0) ? xs(r - 1) : T(0);
-        const T xe = (ix0 + R - 1 < nx - 1) ? xs(r + R) : T(0);
+        in.c = xv(r);
+        in.xw = (ix0 > 0) ? xs(r - 1) : T(0);
+        in.xe = (ix0 + R - 1 < nx - 1) ? xs(r + R) : T(0);
         if (k.preset == MPK_LAPLACE3D) {
             const int64_t nxy = (int64_t)nx * nx;
             const uint32_t iz_ = k.dnxy.div(g);
             const int iy = (int)(q1 - iz_ * (uint32_t)nx), iz = (int)iz_;
+            if (iz > 0) in.pb = xv(r - nxy);
+            if (iy > 0) in.ps = xv(r - nx);
+            if (iy < nx - 1) in.pn = xv(r + nx);
+            if (iz < nx - 1) in.pu = xv(r + nxy);
+            return;
+        }
+        const int iy = (int)q1;
+        if (iy > 0) in.ps = xv(r - nx);
+        if (iy < nx - 1) in.pn = xv(r + nx);
+    }
+    __device__ __forceinline__ void group_eval(int64_t r, const GroupIn &in, T (&out)[R]) const {
+        const uint32_t g = (uint32_t)(k.row0 + r);
+        const int nx = k.nx;
+        const uint32_t q1 = k.dnx.div(g);
+        const int ix0 = (int)(g - q1 * (uint32_t)nx);
+        const Pack<T> &c = in.c;
+        const T xw = in.xw, xe = in.xe;
+        if (k.preset == MPK_LAPLACE3D) {
+            const uint32_t iz_ = k.dnxy.div(g);
+            const int iy = (int)(q1 - iz_ * (uint32_t)nx), iz = (int)iz_;
             const bool B = iz > 0, S = iy > 0, N = iy < nx - 1, U = iz < nx - 1;
-            Pack<T> pb, ps, pn, pu;
-            if (B) pb = xv(r - nxy);
-            if (S) ps = xv(r - nx);
-            if (N) pn = xv(r + nx);
-            if (U) pu = xv(r + nxy);
 #pragma unroll
             for (int e = 0; e < R; ++e) {
                 const int ix = ix0 + e;
                 T acc = T(0);
-                if (B) acc = RN<T>::add(acc, RN<T>::mul(cT[0], pb.v[e]));
-                if (S) acc = RN<T>::add(acc, RN<T>::mul(cT[1], ps.v[e]));
+                if (B) acc = RN<T>::add(acc, RN<T>::mul(cT[0], in.pb.v[e]));
+                if (S) acc = RN<T>::add(acc, RN<T>::mul(cT[1], in.ps.v[e]));
                 if (ix > 0) acc = RN<T>::add(acc, RN<T>::mul(cT[2], e ? c.v[e ? e - 1 : 0] : xw));
                 acc = RN<T>::add(acc, RN<T>::mul(cT[3], c.v[e]));
                 if (ix < nx - 1) acc = RN<T>::add(acc, RN<T>::mul(cT[4], e < R - 1 ? c.v[e < R - 1 ? e + 1 : 0] : xe));
-                if (N) acc = RN<T>::add(acc, RN<T>::mul(cT[5], pn.v[e]));
-                if (U) acc = RN<T>::add(acc, RN<T>::mul(cT[6], pu.v[e]));
+                if (N) acc = RN<T>::add(acc, RN<T>::mul(cT[5], in.pn.v[e]));
+                if (U) acc = RN<T>::add(acc, RN<T>::mul(cT[6], in.pu.v[e]));
                 out[e] = acc;
             }
             return;
         }
         const int iy = (int)q1;
         const bool S = iy > 0, N = iy < nx - 1;
-        Pack<T> ps, pn;
-        if (S) ps = xv(r - nx);
-        if (N) pn = xv(r + nx);
         double pyc = 0.0, py1 = 0.0;
         if (k.preset == MPK_BENTPIPE2D) {
             const double py = __dmul_rn((double)(iy + 1), k.h);
@@ -251,13 +307,19 @@ template <typename T> struct StencilOp {
                 c4 = RN<T>::from_double(__dadd_rn(-1.0, __dmul_rn(k.hh, uy)));
             }
             T acc = T(0);
-            if (S) acc = RN<T>::add(acc, RN<T>::mul(c0, ps.v[e]));
+            if (S) acc = RN<T>::add(acc, RN<T>::mul(c0, in.ps.v[e]));
             if (ix > 0) acc = RN<T>::add(acc, RN<T>::mul(c1, e ? c.v[e ? e - 1 : 0] : xw));
             acc = RN<T>::add(acc, RN<T>::mul(c2, c.v[e]));
             if (ix < nx - 1) acc = RN<T>::add(acc, RN<T>::mul(c3, e < R - 1 ? c.v[e < R - 1 ? e + 1 : 0] : xe));
-            if (N) acc = RN<T>::add(acc, RN<T>::mul(c4, pn.v[e]));
+            if (N) acc = RN<T>::add(acc, RN<T>::mul(c4, in.pn.v[e]));
             out[e] = acc;
         }
+    }
+    template <class XV, class XS>
+    __device__ __forceinline__ void row_group(int64_t r, XV xv, XS xs, T (&out)[R]) const {
+        GroupIn in;
+        group_load(r, xv, xs, in);
+        group_eval(r, in, out);
     }
     // lane-per-row over [r0, r0 + 32) (interface of CsrOp::warp_rows)
     template <class X> __device__ __forceinline__ T warp_rows(int64_t r0, int64_t rend, X x, T *) const {

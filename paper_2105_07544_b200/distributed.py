@@ -465,6 +465,8 @@ def dist_gmres_restarted(sysm: LocalSystem, b, x0, cfg: SolverConfig, norm_basel
     prec = cfg.precision
     if cfg.m + 1 > 52:
         raise ValueError("row-partitioned cycles support m <= 51")
+    if cfg.basis_precision != "working":
+        raise ValueError("row-partitioned cycles keep the basis in the working precision")
     t = D.torch()
     ws = _DistWs(sysm, cfg.m, prec)
     bd = _local_vec(sysm, b, prec.torch_dtype)
@@ -519,6 +521,8 @@ def dist_gmres_ir(sysm: LocalSystem, b, x0, cfg: IrConfig):
         raise ValueError("the device refinement runs fp32 inside fp64")
     if cfg.inner.m + 1 > 52:
         raise ValueError("row-partitioned cycles support m <= 51")
+    if cfg.inner.basis_precision != "working":
+        raise ValueError("row-partitioned cycles keep the basis in the working precision")
     t = D.torch()
     n = sysm.n
     ws = _DistWs(sysm, cfg.inner.m, low)

@@ -42,16 +42,17 @@ class Readout:
 class CycleWorkspace:
     _cache: dict = {}
 
-    def __init__(self, n: int, m: int, prec: Precision):
+    def __init__(self, n: int, m: int, prec: Precision, basis: str = "working"):
         t = D.torch()
         lib = D.lib()
-        self.n, self.m, self.prec = int(n), int(m), prec
+        self.n, self.m, self.prec, self.basis = int(n), int(m), prec, basis
         self.ld = D.ld_for(n)
         td = prec.torch_dtype
         dev = D.device()
         # zero-initialised: rows [n, ld) of every column stay zero (the fused
-        # kernel's 16-byte row groups and chunk tails read them)
-        self.V = t.zeros((self.m + 1) * self.ld, dtype=td, device=dev)
+        # kernel's 16-byte row groups and chunk tails read them).  A binary16
+        # basis (SolverConfig.basis_precision) halves its bytes.
+        self.V = t.zeros((self.m + 1) * self.ld, dtype=t.float16 if basis == "binary16" else td, device=dev)
         # + 512 elements: 1-D bulk copies of a 256-row tile may run past w''s ld
         self.work = t.zeros(4 * self.ld + 512, dtype=td, device=dev)
         self.hess = t.zeros(int(lib.mpk_cycle_hess_bytes(self.m, prec.code)), dtype=t.uint8, device=dev)
@@ -63,13 +64,13 @@ class CycleWorkspace:
         self.flags = 0
 
     @classmethod
-    def get(cls, n, m, prec) -> "CycleWorkspace":
-        key = (D.torch().cuda.current_device(), int(n), int(m), prec)
+    def get(cls, n, m, prec, basis: str = "working") -> "CycleWorkspace":
+        key = (D.torch().cuda.current_device(), int(n), int(m), prec, basis)
         ws = cls._cache.get(key)
         if ws is None:
             if len(cls._cache) > 8:
                 cls._cache.clear()
-            ws = cls._cache[key] = CycleWorkspace(n, m, prec)
+            ws = cls._cache[key] = CycleWorkspace(n, m, prec, basis)
         return ws
 
     # -- pointers into the control buffer ----------------------------------
@@ -93,7 +94,8 @@ class CycleWorkspace:
         _lib.check(D.lib().mpk_dot(prec.code, b.shape[0], D.ptr(b), D.ptr(b), self.at(OFF_BN2),
                                    self.ws.ptr, D.stream()))
 
-    def cycle(self, A, M, r0, rnorm2_off, x0, x_out, steps_cap, exit_tol, norm_scale, rule, orth="cgs2"):
+    def cycle(self, A, M, r0, rnorm2_off, x0, x_out, steps_cap, exit_tol, norm_scale, rule, orth="cgs2",
+              basis="working"):
         """Enqueue one whole cycle (gmres.py:134-205) via mpk_cycle_run."""
         d = self.desc
         self._pins = [A.descriptor()]
@@ -122,7 +124,9 @@ class CycleWorkspace:
         d.ws = self.ws.ptr
         d.ctl = self.ctl_ptr
         d.nranks = 1
-        d.flags = self.flags | (16 if orth == "dcgs2" else 0)
+        if basis != self.basis:
+            raise ValueError("workspace holds a %s basis, cycle asked for %s" % (self.basis, basis))
+        d.flags = self.flags | (16 if orth == "dcgs2" else 0) | (32 if basis == "binary16" else 0)
         _lib.check(D.lib().mpk_cycle_run(ctypes.byref(d), D.stream()))
 
     # -- readback -----------------------------------------------------------

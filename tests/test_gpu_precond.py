@@ -148,3 +148,60 @@ def test_jacobi1_fused_cycle_matches_multikernel_and_oracle(cuda):
     inner = mk.SolverConfig(m=50, rtol=1e-4, precision=P.binary32, max_iters=5000)
     ir = mk.gmres_ir(A, b, np.zeros(A.n), mk.IrConfig(inner=inner, rtol=1e-10), M=J32, A_low=Al)
     assert ir.converged and ir.final_explicit_relres <= 1e-10
+
+
+@pytest.mark.parametrize("k,prec", [(1, P.binary64), (5, P.binary64), (16, P.binary32), (42, P.binary64),
+                                    (64, P.binary32)])
+def test_device_block_lu_matches_lapack(cuda, rng, k, prec):
+    """mpk_block_lu (device setup) vs the oracle's scipy.linalg.lu_factor
+    (preconditioners.py:96-130): same pivot rows, factors equal to rounding,
+    P L U reconstructing each block, thresholds equal."""
+    from conftest import random_csr
+
+    n = 3 * k + (k // 2 if k > 1 else 0) + 1
+    A, dense = random_csr(mk, rng, n, diag_shift=0.0)   # real pivoting
+    M = mk.build_block_jacobi(A, k, precision=prec)
+    ref = O.jacobi_build(A.row_ptr, A.col_idx, A.values, k, prec.dtype)
+    tol = 1e-12 if prec is P.binary64 else 2e-5
+    assert M.data.num_blocks == len(ref.factors)
+    for bi, ((lu, piv), (rlu, rpiv)) in enumerate(zip(M.data.factors, ref.factors)):
+        assert lu.shape == rlu.shape and lu.dtype == prec.dtype
+        assert np.array_equal(piv, rpiv), bi
+        scale = np.abs(rlu).max()
+        assert np.abs(lu.astype(np.float64) - rlu).max() <= tol * 10 * scale * lu.shape[0], bi
+    # the apply: equal to the oracle's lu_solve with the reference factors to rounding
+    v = rng.standard_normal(n).astype(prec.dtype)
+    got = M.apply(v)
+    want = ref(v)
+    assert np.allclose(got, want, rtol=tol * 100, atol=tol * 100 * np.abs(want).max())
+
+
+def test_device_block_lu_singular_matches_reference_rule(cuda):
+    """The pivot test pivot <= kb*u*max row sum names the same block as the
+    reference (SingularBlockError(block, pivot, threshold))."""
+    # block 2 (rows 4-5) exactly singular, block 1 nearly singular but above the threshold
+    rows = np.array([0, 1, 2, 2, 3, 3, 4, 4, 5, 5])
+    cols = np.array([0, 1, 2, 3, 2, 3, 4, 5, 4, 5])
+    vals = np.array([1.0, 2.0, 1.0, 1.0, 1.0, 1.0 + 1e-9, 1.0, 2.0, 2.0, 4.0])
+    A = mk.csr_from_coo(rows, cols, vals, 6)
+    with pytest.raises(mk.SingularBlockError) as info:
+        mk.build_block_jacobi(A, 2)
+    try:
+        O.jacobi_build(A.row_ptr, A.col_idx, A.values, 2, np.float64)
+    except ValueError as e:
+        _, bi, pv, lim = e.args
+    assert info.value.block_index == bi == 2
+    assert info.value.threshold == lim
+    assert info.value.pivot == pv == 0.0
+
+
+def test_device_block_lu_large_batch(cuda):
+    """C5-shaped setup (jacobi:42 over a banded irregular CSR): every block's
+    apply equals the dense solve to rounding."""
+    A = mk.synthetic_irregular(20000, signs="negative", dominance=1.001, shift=1e-3, far_frac=0.01, band=200)
+    M = mk.build_block_jacobi(A, 42)
+    v = np.random.default_rng(5).standard_normal(A.n)
+    got = M.apply(v)
+    ref = O.jacobi_build(A.row_ptr, A.col_idx, A.values, 42, np.float64)
+    want = ref(v)
+    assert np.abs(got - want).max() <= 1e-10 * np.abs(want).max()

@@ -126,3 +126,14 @@ def test_precision_parsing():
         mk.Precision.parse("half")
     with pytest.raises(mk.PrecisionMismatchError):
         mk.Precision.from_dtype(np.int32)
+
+
+def test_binary16_basis_validation():
+    with pytest.raises(ValueError):
+        mk.SolverConfig(precision=mk.Precision.binary64, basis_precision="binary16")
+    with pytest.raises(ValueError):
+        mk.SolverConfig(precision=mk.Precision.binary32, m=60, basis_precision="binary16")
+    with pytest.raises(ValueError):
+        mk.SolverConfig(precision=mk.Precision.binary32, orthogonalization="dcgs2", basis_precision="binary16")
+    with pytest.raises(ValueError):
+        mk.SolverConfig(basis_precision="bfloat16")

@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(NT, 1) k_reg(const float *V, int64_t ld, int n
     const int64_t rb = blockIdx.x * rpc, re = rb + rpc < n ? rb + rpc : n;
     constexpr int KU = KUX ? KUX : KP / U;
     constexpr int64_t TRIP = 32 * U;
-    float acc[KP];
+    float acc[KU > KP ? KU : KP];
 #pragma unroll
     for (int i = 0; i < KP; ++i) acc[i] = 0.f;
     float cf[KU];
@@ -319,6 +319,11 @@ static CUtensorMap make_map(const float *V, int64_t ld, int nc, int TR) {
     return m;
 }
 
+template <int U, int KU> void launch_reg(int sms, const float *V, int64_t ld, int nc, int64_t n, const float *x,
+                                         float *y, const float *coef, float *part, int rev) {
+    k_reg<U, 0, KU><<<sms, NT>>>(V, ld, nc, n, x, y, coef, part, rev);
+}
+
 int main() {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -330,71 +335,53 @@ int main() {
         cudaMalloc(&y, ld * 4 + 4096);
         cudaMalloc(&coef, 64 * 4);
         cudaMalloc(&part, 64 * 4 * 320);
-        std::vector<float> h(ld);
-        for (int64_t i = 0; i < ld; ++i) h[i] = (float)((i * 2654435761u) % 1000) * 1e-3f;
-        for (int c = 0; c < 52; ++c) cudaMemcpy(V + c * ld, h.data(), ld * 4, cudaMemcpyHostToDevice);
-        cudaMemcpy(x, h.data(), ld * 4, cudaMemcpyHostToDevice);
-        std::vector<float> hc(64, 0.01f);
-        cudaMemcpy(coef, hc.data(), 64 * 4, cudaMemcpyHostToDevice);
-        cudaFuncSetAttribute(k_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRing);
-        cudaFuncSetAttribute(k_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRing);
-        cudaFuncSetAttribute(k_tma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRing);
-        cudaFuncSetAttribute(k_tma2d<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRing);
-        cudaFuncSetAttribute(k_tma2d<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRing);
+        cudaMemset(V, 0, ld * 52 * 4);
+        cudaMemset(x, 0, ld * 4);
+        cudaMemset(coef, 0, 64 * 4);
         cudaEvent_t a, b;
         cudaEventCreate(&a);
         cudaEventCreate(&b);
-        std::vector<float> pr(64 * sms), pt(64 * sms);
-        for (int nc : {26, 28, 32, 36, 40, 44}) {
-            auto reg = [&](int rev) {
-                if (nc * 4 <= 13 * 4 && (nc + 3) / 4 * 4 <= 13) k_reg<4><<<sms, NT>>>(V, ld, nc, n, x, y, coef, part, rev);
-                else if ((nc + 3) / 4 * 2 <= 13) k_reg<2><<<sms, NT>>>(V, ld, nc, n, x, y, coef, part, rev);
-                else k_reg<1><<<sms, NT>>>(V, ld, nc, n, x, y, coef, part, rev);
+        for (int nc = 1; nc <= 51; ++nc) {
+            const int ncp = (nc + 3) / 4;
+            auto cur = [&](int rev) {
+                if (ncp * 8 <= 13) launch_reg<8, 1>(sms, V, ld, nc, n, x, y, coef, part, rev);
+                else if (ncp * 4 <= 13) launch_reg<4, 3>(sms, V, ld, nc, n, x, y, coef, part, rev);
+                else if (ncp * 2 <= 13) launch_reg<2, 6>(sms, V, ld, nc, n, x, y, coef, part, rev);
+                else launch_reg<1, 13>(sms, V, ld, nc, n, x, y, coef, part, rev);
             };
-            auto regpf = [&](int rev, int pf) {
-#define PFV(PFR)                                                                                          \
-    if ((nc + 3) / 4 * 4 <= 13) k_reg<4, PFR><<<sms, NT>>>(V, ld, nc, n, x, y, coef, part, rev);         \
-    else if ((nc + 3) / 4 * 2 <= 13) k_reg<2, PFR><<<sms, NT>>>(V, ld, nc, n, x, y, coef, part, rev);    \
-    else k_reg<1, PFR><<<sms, NT>>>(V, ld, nc, n, x, y, coef, part, rev);
-                if (pf == 1024) { PFV(1024) } else if (pf == 2048) { PFV(2048) } else { PFV(4096) }
-            };
-            const CUtensorMap m128 = make_map(V, ld, nc, 128), m256 = make_map(V, ld, nc, 256);
-            auto tma = [&](int rev) {
-                if (nc <= 24) k_tma2d<256><<<sms, NT, kRing>>>(m256, V, ld, nc, n, x, y, coef, part, rev);
-                else k_tma2d<128><<<sms, NT, kRing>>>(m128, V, ld, nc, n, x, y, coef, part, rev);
+            auto best = [&](int rev) {
+                switch (ncp) {
+                    case 1: launch_reg<12, 1>(sms, V, ld, nc, n, x, y, coef, part, rev); break;
+                    case 2: launch_reg<6, 2>(sms, V, ld, nc, n, x, y, coef, part, rev); break;
+                    case 3: launch_reg<4, 3>(sms, V, ld, nc, n, x, y, coef, part, rev); break;
+                    case 4: launch_reg<3, 4>(sms, V, ld, nc, n, x, y, coef, part, rev); break;
+                    case 5: launch_reg<3, 5>(sms, V, ld, nc, n, x, y, coef, part, rev); break;
+                    case 6: launch_reg<2, 6>(sms, V, ld, nc, n, x, y, coef, part, rev); break;
+                    case 7: launch_reg<2, 7>(sms, V, ld, nc, n, x, y, coef, part, rev); break;
+                    case 8: launch_reg<2, 8>(sms, V, ld, nc, n, x, y, coef, part, rev); break;
+                    case 9: launch_reg<2, 9>(sms, V, ld, nc, n, x, y, coef, part, rev); break;
+                    case 10: launch_reg<1, 10>(sms, V, ld, nc, n, x, y, coef, part, rev); break;
+                    case 11: launch_reg<1, 11>(sms, V, ld, nc, n, x, y, coef, part, rev); break;
+                    case 12: launch_reg<1, 12>(sms, V, ld, nc, n, x, y, coef, part, rev); break;
+                    default: launch_reg<1, 13>(sms, V, ld, nc, n, x, y, coef, part, rev); break;
+                }
             };
             const double bytes = (double)n * 4 * (nc + 2);
-            for (int impl = 0; impl < 4; ++impl) {
-                for (int serp = 1; serp < 2; ++serp) {
-                    auto run = [&](int i) {
-                        const int rv = serp ? (i & 1) : 0;
-                        const int ncp = (nc + 3) / 4;
-                        if (impl == 0) reg(rv);
-                        else if (impl == 1) { if (ncp <= 7) k_reg<2, 0, 7><<<sms, NT>>>(V, ld, nc, n, x, y, coef, part, rv); else if (ncp <= 8) k_reg<2, 0, 8><<<sms, NT>>>(V, ld, nc, n, x, y, coef, part, rv); else if (ncp <= 9) k_reg<2, 0, 9><<<sms, NT>>>(V, ld, nc, n, x, y, coef, part, rv); else k_reg<2, 0, 11><<<sms, NT>>>(V, ld, nc, n, x, y, coef, part, rv); }
-                        else if (impl == 2) { if (ncp <= 7) k_reg<1, 0, 7><<<sms, NT>>>(V, ld, nc, n, x, y, coef, part, rv); else if (ncp <= 8) k_reg<1, 0, 8><<<sms, NT>>>(V, ld, nc, n, x, y, coef, part, rv); else if (ncp <= 9) k_reg<1, 0, 9><<<sms, NT>>>(V, ld, nc, n, x, y, coef, part, rv); else k_reg<1, 0, 11><<<sms, NT>>>(V, ld, nc, n, x, y, coef, part, rv); }
-                        else reg(rv);
-                    };
-                    for (int i = 0; i < 3; ++i) run(i);
-                    cudaEventRecord(a);
-                    const int R = 20;
-                    for (int i = 0; i < R; ++i) run(i);
-                    cudaEventRecord(b);
-                    cudaEventSynchronize(b);
-                    float ms;
-                    cudaEventElapsedTime(&ms, a, b);
-                    printf("n=%8lld nc=%2d %s serp=%d : %7.2f us  %7.1f GB/s  (%s)\n", (long long)n, nc,
-                           impl == 0 ? "reg" : impl == 1 ? "U2KUexact" : impl == 2 ? "U1KUexact" : "reg", serp, ms * 1e3 / R, bytes * R / ms / 1e6,
-                           cudaGetErrorString(cudaGetLastError()));
-                }
-                cudaMemcpy(impl ? pt.data() : pr.data(), part, 64 * 4 * sms, cudaMemcpyDeviceToHost);
+            double gbs[2];
+            for (int impl = 0; impl < 2; ++impl) {
+                auto run = [&](int i) { impl ? best(i & 1) : cur(i & 1); };
+                for (int i = 0; i < 3; ++i) run(i);
+                cudaEventRecord(a);
+                const int R = 20;
+                for (int i = 0; i < R; ++i) run(i);
+                cudaEventRecord(b);
+                cudaEventSynchronize(b);
+                float ms;
+                cudaEventElapsedTime(&ms, a, b);
+                gbs[impl] = bytes * R / ms / 1e6;
             }
-            double md = 0;
-            for (int c = 0; c < nc; ++c) {
-                double sa = 0, sb = 0;
-                for (int k = 0; k < sms; ++k) sa += pr[c * sms + k], sb += pt[c * sms + k];
-                md = fmax(md, fabs(sa - sb) / (fabs(sa) + 1e-30));
-            }
-            printf("   dots reg vs tma max rel diff %.3e\n", md);
+            printf("n=%8lld nc=%2d cur %7.1f GB/s  best %7.1f GB/s  (%s)\n", (long long)n, nc, gbs[0], gbs[1],
+                   cudaGetErrorString(cudaGetLastError()));
         }
         cudaFree(V); cudaFree(x); cudaFree(y); cudaFree(coef); cudaFree(part);
     }
