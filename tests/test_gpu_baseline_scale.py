@@ -52,12 +52,13 @@ def test_c2_gmres_ir_matches_reference_run(bentpipe):
     inner = mk.SolverConfig(m=50, rtol=1e-4, precision=P.binary32, max_iters=100000)
     rep = mk.gmres_ir(A, np.ones(A.n), np.zeros(A.n), mk.IrConfig(inner=inner, rtol=1e-10))
     assert rep.converged and rep.final_explicit_relres <= 1e-10
-    # fp32 inner cycles make the count chaotic in the last bit: this solver
-    # gives 10400-10800 for 148/144/128/100/74 CTAs (reduction orders,
-    # profiles/r02_C2_ir_spread.json) around the reference's 10650 (8
-    # OpenBLAS threads); hold it to that spread
-    assert abs(rep.total_iters - ref["iters"]) <= 300, (rep.total_iters, ref["iters"])
-    assert abs(rep.restarts - ref["restarts"]) <= 6
+    # fp32 inner cycles make the count chaotic in the last bit: the
+    # reference itself gives 10250 (1 OpenBLAS thread, big/c2_ir_t1.npz) and
+    # 10650 (8 threads, runs.json); this solver 10400-10800 for
+    # 148/144/128/100/74 CTAs (profiles/r02_C2_ir_spread.json).  Hold the
+    # count to the reference's spread widened by one restart cycle.
+    counts = [int(ref["iters"])] + [int(g["iters"]) for g in big("c2_ir")]
+    assert min(counts) - 50 <= rep.total_iters <= max(counts) + 50, (rep.total_iters, counts)
     ours = explicit(rep, "outer")
     theirs = np.array([r[3] for r in ref["history"] if r[1] == "outer"])
     k = min(len(ours), len(theirs))
@@ -122,3 +123,24 @@ def test_c4_fp64_gmres_matches_reference_run(laplace200):
         gi = g["h_impl"]
         m = ~np.isnan(gi) & ~np.isnan(impl)
         assert np.abs(impl[m] / gi[m] - 1).max() <= 1e-4
+
+
+def test_c4_gmres_ir_matches_reference_runs(laplace200):
+    """C4 GMRES-IR(50), breakdown rule "u", vs the reference's
+    own runs with that rule (make_big_golden.py c4_ir_u, 1 and 4 OpenBLAS
+    threads): identical counts (4100 iterations, 82 refinements = the paper's
+    Trilinos count), per-refinement explicit residuals within 1e-2 relative
+    (fp32 inner cycles; observed 1.5e-3, reference t1 vs t4 9e-5)."""
+    runs = big("c4_ir_u")
+    assert runs, "missing tests/golden/big/c4_ir_u_t*.npz"
+    A = laplace200
+    inner = mk.SolverConfig(m=50, rtol=1e-4, precision=P.binary32, max_iters=100000, breakdown_rule="u")
+    rep = mk.gmres_ir(A, np.ones(A.n), np.zeros(A.n), mk.IrConfig(inner=inner, rtol=1e-10))
+    assert rep.converged and rep.final_explicit_relres <= 1e-10
+    ours = explicit(rep, "outer")
+    for g in runs:
+        assert rep.total_iters == int(g["iters"]) and rep.restarts == int(g["restarts"])
+        theirs = g["h_expl"][g["h_phase"] == 2]
+        assert len(ours) == len(theirs)
+        rel = np.abs(ours / theirs - 1)
+        assert rel[:7].max() <= 1e-4 and rel.max() <= 1e-2, (rel[:7].max(), rel.max())
