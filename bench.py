@@ -518,6 +518,19 @@ def main():
         msfd, repfd = timed(solve_fd, 1)
         out["fd"] = {"switch_iter": args.fd, "s": msfd / 1e3, "iters": repfd[-1].total_iters,
                      "converged": bool(repfd[-1].converged)}
+    if args.poly and world == 1:
+        # the same IR solve with the polynomial on the multi-kernel cycle
+        # (desc flag 4: one launch per SpMV / update) -- what fusing the
+        # polynomial into the persistent kernel bought
+        wsi.flags = 4
+        try:
+            solve_ir(b_dev, x0_dev)
+            msmk, repsmk = timed(lambda: solve_ir(b_dev, x0_dev), 1)
+        finally:
+            wsi.flags = 0
+        out["poly_multikernel"] = {"ir_s": msmk / 1e3, "iters": repsmk[-1].total_iters,
+                                   "us_per_iter": msmk * 1e3 / max(repsmk[-1].total_iters, 1),
+                                   "fused_speedup": msmk / ms_step}
     if args.config == "C5":
         out["details"]["precond"] = {"kind": "block-jacobi", "block": 1, "fused": "diagonal scaling in k_cycle_reg"}
         out["details"]["operator"] = "CSR, warp-cooperative bit-exact rows"

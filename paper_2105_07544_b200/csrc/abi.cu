@@ -278,6 +278,16 @@ template <typename T> int64_t csr_window_elems(const CsrOp<T> &op, int64_t rows)
     return e * (int64_t)sizeof(T) <= kWinMaxBytes ? e : 0;
 }
 
+// Two descriptors of the same operator (the polynomial's matrix and the
+// cycle's): same kind, size, and storage or stencil definition.
+bool same_operator(const mpk_matrix *a, const mpk_matrix *b) {
+    if (a == b) return true;
+    if (a->kind != b->kind || a->dtype != b->dtype || a->n != b->n || a->row0 != b->row0) return false;
+    if (a->kind == MPK_CSR) return a->row_ptr == b->row_ptr && a->col_idx == b->col_idx && a->values == b->values;
+    return a->preset == b->preset && a->nx == b->nx && a->diffusion == b->diffusion && a->velocity == b->velocity &&
+           a->convection == b->convection && a->stretch == b->stretch;
+}
+
 template <typename T, class F> int with_op(const mpk_matrix *A, F &&f) {
     if (A->kind == MPK_STENCIL) return f(make_stencil<T>(A));
     if (A->kind == MPK_CSR) return f(make_csr<T>(A));
@@ -652,6 +662,38 @@ int launch_fused_reg(const Op &op, const mpk_cycle_desc *d, int cap, double tf, 
     fa.diag = nullptr;
     fa.z = w + 3 * d->ld;
     fa.csr_win = win > 0 ? 1 : 0;
+    if (d->M && d->M->kind == MPK_PC_POLY) {
+        // units of the product form with the multi-kernel path's host
+        // arithmetic (apply_precond_t): inv = 1/re; tr = 2 re, m2 = re^2 + im^2
+        const mpk_precond *M = d->M;
+        int nu = 0;
+        for (int i = 0; i < M->degree;) {
+            if (nu >= kMaxPolyUnits) return fail(MPK_EUNSUPPORTED, "polynomial degree too high for the fused cycle");
+            const double re = M->roots_re[i], im = M->roots_im[i];
+            if (im == 0.0) {
+                fa.poly[nu].pair = 0;
+                fa.poly[nu].a = (T)(1.0 / re);
+                fa.poly[nu].b = T(0);
+                i += 1;
+            } else {
+                volatile double tr = 2.0 * re;
+                volatile double rr = re * re;
+                volatile double ii = im * im;
+                const double m2 = rr + ii;
+                fa.poly[nu].pair = 1;
+                fa.poly[nu].a = (T)tr;
+                fa.poly[nu].b = (T)m2;
+                i += 2;
+            }
+            ++nu;
+        }
+        fa.npoly = nu;
+        const int64_t pn = M->n;
+        fa.pw0 = (T *)M->work;
+        fa.pw1 = fa.pw0 + pn;
+        fa.pt = fa.pw1 + pn;
+        fa.pacc = w + 3 * d->ld;
+    }
     if constexpr (half) {
         const double e = std::nearbyint(0.5 * std::log2((double)(d->n > 1 ? d->n : 1)));
         fa.vs = (T)std::ldexp(1.0, (int)e);
@@ -756,11 +798,15 @@ template <typename T> int run_cycle(const mpk_cycle_desc *d, cudaStream_t s) {
     int rc;
 
     if (d->nranks > 1) {
-        if (precond || m + 1 > kRegMaxCols || (uintptr_t)d->x_out % 16 || (uintptr_t)d->V % 16 ||
+        // identity, or block Jacobi(1) whose `lu` is the GLOBAL diagonal
+        // offset to the rank's first row (halo rows read their own a_ii)
+        const bool jac1 = precond && d->M->kind == MPK_PC_JACOBI && d->M->block == 1 && d->M->n == n &&
+                          d->M->dtype == d->dtype && (uintptr_t)d->M->lu % 16 == 0;
+        if ((precond && !jac1) || m + 1 > kRegMaxCols || (uintptr_t)d->x_out % 16 || (uintptr_t)d->V % 16 ||
             (uintptr_t)d->work % 16 || (uintptr_t)d->r0 % 16)
-            return fail(MPK_EUNSUPPORTED, "row-partitioned cycle: identity preconditioner, m <= 51, "
+            return fail(MPK_EUNSUPPORTED, "row-partitioned cycle: identity or Jacobi(1) preconditioner, m <= 51, "
                                           "16-byte aligned buffers");
-        if (d->flags & 16)   // lagged one-reduction CGS2, row-partitioned instantiation
+        if ((d->flags & 16) && !precond)   // lagged one-reduction CGS2, row-partitioned instantiation
             return with_op<T>(d->A, [&](auto op) -> int { return launch_dcgs2<T, decltype(op)>(op, d, cap, tf, u, s); });
         return with_op<T>(d->A, [&](auto op) -> int {
             return launch_fused_reg<T, decltype(op)>(op, d, cap, tf, u, s);
@@ -794,6 +840,17 @@ template <typename T> int run_cycle(const mpk_cycle_desc *d, cudaStream_t s) {
     // blocks beyond 51 columns)
     if (!precond && !(d->flags & 4) && (uintptr_t)d->x_out % 16 == 0 &&
         (uintptr_t)d->V % 16 == 0 && (uintptr_t)d->work % 16 == 0 && (uintptr_t)d->r0 % 16 == 0) {
+        return with_op<T>(d->A, [&](auto op) -> int {
+            return launch_fused_reg<T, decltype(op)>(op, d, cap, tf, u, s);
+        });
+    }
+    // GMRES polynomial on the cycle's own operator: applied inside the
+    // persistent register kernel (one grid barrier per SpMV)
+    const bool poly_fused = precond && d->M->kind == MPK_PC_POLY && d->M->dtype == d->dtype && d->M->n == n &&
+                            d->nranks <= 1 && m + 1 <= kRegMaxCols && !(d->flags & 4) && d->M->work &&
+                            d->M->poly_A && same_operator(d->M->poly_A, d->A);
+    if (poly_fused && (uintptr_t)d->x_out % 16 == 0 && (uintptr_t)d->V % 16 == 0 &&
+        (uintptr_t)d->work % 16 == 0 && (uintptr_t)d->r0 % 16 == 0 && (uintptr_t)d->M->work % 16 == 0) {
         return with_op<T>(d->A, [&](auto op) -> int {
             return launch_fused_reg<T, decltype(op)>(op, d, cap, tf, u, s);
         });
@@ -966,15 +1023,12 @@ int mpk_spmv(const mpk_matrix *A, const void *x, void *y, void *stream) {
                 if (we > 0) {
                     // banded rows: x window in shared memory; 16 entries per
                     // lane when rows are long (config 5: ~49 entries)
-                    const bool wide = op.v != nullptr && A->nnz > 16 * A->n;
-                    auto kw = wide ? k_spmv_win<T, 16> : k_spmv_win<T, 8>;
+                    auto kw = k_spmv_win<T, 8>;   // gathers hit shared memory: 8 entries per lane suffice
                     const size_t smem = (size_t)we * sizeof(T);
                     // the window replaces L1 reuse: prefer shared memory so
                     // occupancy is not capped by the default carveout
                     static bool carve = false;
                     if (!carve) {
-                        cudaFuncSetAttribute(k_spmv_win<T, 16>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                             (int)cudaSharedmemCarveoutMaxShared);
                         cudaFuncSetAttribute(k_spmv_win<T, 8>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                              (int)cudaSharedmemCarveoutMaxShared);
                         carve = true;

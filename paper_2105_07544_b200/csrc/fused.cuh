@@ -42,6 +42,15 @@ template <typename T> struct CommArgs {
     int64_t mir_lo[kMaxRanks], mir_hi[kMaxRanks];   // own local rows mirrored into rank q's xg
 };
 
+// GMRES-polynomial preconditioner inside the persistent cycle
+// (apply_gmres_poly, preconditioners.py:276-305): one unit per real root
+// (a = 1/theta) or conjugate pair (a = 2 Re theta, b = |theta|^2), Leja order.
+constexpr int kMaxPolyUnits = 32;
+template <typename T> struct PolyUnit {
+    int pair;
+    T a, b;
+};
+
 template <typename T> struct FusedArgs {
     int64_t n, ld;
     int m, cap;
@@ -63,6 +72,21 @@ template <typename T> struct FusedArgs {
     T *z;             // k_cycle_reg: z = v_k / a_ii for the CTA's own rows
     int csr_win = 0;  // k_cycle_reg: banded CSR, x window after the staging buffers (1024 + 2*band elements)
     T vs = T(1), vsi = T(1);   // k_cycle_reg, binary16 basis: stored = v * vs (power of two), vsi = 1 / vs
+    // k_cycle_reg with a GMRES-polynomial right preconditioner (npoly > 0):
+    // z = p(A) v_k and the correction's p(A) (V_k d) evaluated in-kernel,
+    // one grid barrier per SpMV; pw0/pw1 ping-pong the product-form work
+    // vector, pt the pair temporary, pacc the accumulator (z)
+    int npoly = 0;
+    PolyUnit<T> poly[kMaxPolyUnits];
+    T *pw0 = nullptr, *pw1 = nullptr, *pt = nullptr, *pacc = nullptr;
+};
+
+// x accessor over a global vector written by other CTAs of this persistent
+// kernel (after a grid barrier): L2 loads, never a stale L1 line
+template <typename T> struct XCG {
+    const T *p;
+    __device__ __forceinline__ T operator()(int64_t c) const { return __ldcg(p + c); }
+    __device__ __forceinline__ Pack<T> vec(int64_t c) const { return ldcg16(p + c); }
 };
 
 // Phase profiler (desc flag bit 3): per-CTA clock64 totals of each section,

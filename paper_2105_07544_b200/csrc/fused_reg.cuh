@@ -82,7 +82,7 @@ __device__ __forceinline__ void reg_phase_u(const TV *V, int64_t ld, int nc, int
             if (MODE == kRegCorrect) {
 #pragma unroll
                 for (int e = 0; e < R; ++e)
-                    xv[u][e] = (p == 0 && live && r + e < n) ? x[r + e] : T(0);   // x may alias y
+                    xv[u][e] = (x != nullptr && p == 0 && live && r + e < n) ? x[r + e] : T(0);   // x may alias y; null: 0
             } else if (MODE == kRegUpdateNorm && p != 0) {
 #pragma unroll
                 for (int e = 0; e < R; ++e) xv[u][e] = T(0);   // only part 0 uses x (x may alias y)
@@ -293,9 +293,10 @@ __device__ __noinline__ T phase_a_spmv(const Op &A, const XS xs, T *w, int64_t r
         // 16-byte row groups: vector reads of the group and its S/N (B/U)
         // neighbours; UG groups per thread per trip with every group's loads
         // issued before any is evaluated (||w||^2 summed in row order as
-        // with one group per trip)
+        // with one group per trip).  UG = 4 spilled (Laplace3D: 5 packs per
+        // group) and cost 18% of the C4 cycle; 2 keeps the loads in registers
         constexpr int R = RegCfg<T>::R;
-        constexpr int UG = 4;
+        constexpr int UG = 2;
         auto xv = [&](int64_t c) { return xs.vec(c); };
         constexpr int64_t S = (int64_t)kFB * R;
         int64_t r = rb + (int64_t)threadIdx.x * R;
@@ -342,6 +343,113 @@ __device__ __noinline__ T phase_a_spmv(const Op &A, const XS xs, T *w, int64_t r
     return an;
 }
 
+// y = A x over the CTA's rows [rb, re) (x read through L2 from a vector the
+// whole grid wrote before the last barrier); fn(r, y_r) on the thread that
+// evaluated row r.  The row -> thread map is the same on every call, so fn
+// may read-modify-write per-row state without a barrier.  Same row sums as
+// the standalone SpMV (row_group == row(); CSR warp_rows == row()).
+template <typename T, class Op, class F>
+__device__ __forceinline__ void cta_rows(const Op &A, const T *x, int64_t rb, int64_t re, T *sstage, F &&fn) {
+    const XCG<T> xs{x};
+    if constexpr (!Op::kStencil) {
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        T *sb = sstage + warp * kCsrWarpBuf;
+        for (int64_t r0 = rb + (int64_t)warp * 32; r0 < re; r0 += (int64_t)kFW * 32) {
+            const T y = A.template warp_rows<8>(r0, re, xs, sb);
+            if (r0 + lane < re) fn(r0 + lane, y);
+        }
+    } else if (A.group_ok()) {
+        constexpr int R = RegCfg<T>::R;
+        auto xv = [&](int64_t c) { return xs.vec(c); };
+        const int64_t rv = rb + (re - rb) / R * R;
+        for (int64_t r = rb + (int64_t)threadIdx.x * R; r < rv; r += (int64_t)kFB * R) {
+            T o[R];
+            A.row_group(r, xv, xs, o);
+#pragma unroll
+            for (int e = 0; e < R; ++e) fn(r + e, o[e]);
+        }
+        for (int64_t r = rv + threadIdx.x; r < re; r += kFB) fn(r, A.row(r, xs));
+    } else {
+        for (int64_t r = rb + threadIdx.x; r < re; r += kFB) fn(r, A.row(r, xs));
+    }
+}
+
+// Buffers of the in-kernel GMRES polynomial (single GPU): units in shared
+// memory, vectors in global memory.
+template <typename T> struct PolyBufs {
+    const PolyUnit<T> *unit;   // shared memory copy of FusedArgs::poly
+    int npoly;
+    T *w0, *w1, *t, *acc;
+    unsigned *bar;
+};
+
+// z = p(A) v for the CTA's rows into pb.acc: apply_gmres_poly's product form
+// (preconditioners.py:283-305) with the same per-row roundings as
+// k_poly_real / k_poly_pair1 / k_poly_pair2 and one grid barrier before
+// every SpMV after the first (`v` must be complete on every CTA).  Out of
+// line so its register needs stay out of the streaming phases.
+template <typename T, class Op>
+__device__ __noinline__ void poly_apply_dev(const Op &A, PolyBufs<T> pb, const T *v, int64_t rb, int64_t re,
+                                            T *sstage) {
+    const T *work = v;
+    T *const wbuf[2] = {pb.w0, pb.w1};
+    int wi = 0;
+    const unsigned nb = gridDim.x;
+    for (int u = 0; u < pb.npoly; ++u) {
+        const PolyUnit<T> pu = pb.unit[u];
+        const bool first = (u == 0), last = (u + 1 == pb.npoly);
+        T *wnext = wbuf[wi];
+        T *acc = pb.acc;
+        if (!pu.pair) {
+            const T inv = pu.a;
+            if (last) {
+                for (int64_t r = rb + threadIdx.x; r < re; r += kFB)
+                    acc[r] = RN<T>::add(first ? T(0) : acc[r], RN<T>::mul(inv, __ldcg(work + r)));
+            } else {
+                cta_rows<T>(A, work, rb, re, sstage, [&](int64_t r, T y) {
+                    const T wr = __ldcg(work + r);
+                    acc[r] = RN<T>::add(first ? T(0) : acc[r], RN<T>::mul(inv, wr));
+                    wnext[r] = RN<T>::sub(wr, RN<T>::mul(inv, y));
+                });
+            }
+        } else {
+            const T tr = pu.a, m2 = pu.b;
+            T *t = pb.t;
+            cta_rows<T>(A, work, rb, re, sstage, [&](int64_t r, T tv) {
+                t[r] = tv;
+                const T q = RN<T>::div(RN<T>::sub(RN<T>::mul(tr, __ldcg(work + r)), tv), m2);
+                acc[r] = RN<T>::add(first ? T(0) : acc[r], q);
+            });
+            if (!last) {
+                __syncthreads();
+                grid_sync(pb.bar, nb);
+                cta_rows<T>(A, t, rb, re, sstage, [&](int64_t r, T sv) {
+                    const T q = RN<T>::div(RN<T>::sub(RN<T>::mul(tr, __ldcg(t + r)), sv), m2);
+                    wnext[r] = RN<T>::sub(__ldcg(work + r), q);
+                });
+            }
+        }
+        if (!last) {
+            __syncthreads();
+            grid_sync(pb.bar, nb);
+            work = wnext;
+            wi ^= 1;
+        }
+    }
+}
+
+// w = A z over the CTA's rows (z = the polynomial's accumulator, complete on
+// every CTA); returns the thread's part of ||w||^2
+template <typename T, class Op>
+__device__ __noinline__ T poly_spmv_dev(const Op &A, const T *z, T *w, int64_t rb, int64_t re, T *sstage) {
+    T an = T(0);
+    cta_rows<T>(A, z, rb, re, sstage, [&](int64_t r, T y) {
+        w[r] = y;
+        an += y * y;
+    });
+    return an;
+}
+
 template <typename T, class Op, bool BIG, bool MULTI, typename TV = T>
 __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
     using C = RegCfg<T>;
@@ -369,6 +477,7 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
     T *swin = a.csr_win ? sstage + kFW * kCsrWarpBuf : nullptr;   // banded CSR x window
     const int xslot = big ? m + 1 : kFExtra;   // partial slot of the extra scalar
     __shared__ T s_gamma, s_beta, s_bn2;
+    __shared__ PolyUnit<T> s_poly[kMaxPolyUnits];
     __shared__ int s_done, s_steps, s_break, s_app;
     __shared__ double s_scale;
 
@@ -420,6 +529,10 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
         return;                                    \
     }
 
+    if (tid < a.npoly) s_poly[tid] = a.poly[tid];
+    // built at the (rare) use sites from the kernel parameters: a struct
+    // live across the cycle would cost the streaming phases registers
+#define MPK_POLY_BUFS PolyBufs<T>{s_poly, a.npoly, a.pw0, a.pw1, a.pt, a.pacc, a.bar}
     if (tid == 0) {
         const T gamma = RN<T>::sqrt_(__ldcg(a.rnorm2));
         s_gamma = gamma;
@@ -510,7 +623,17 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
         }
         MPK_MARK(0);
         __syncthreads();
-        an = phase_a_spmv<T>(A, XSlab<T, TV>{src, vk, dv, rb, re, a.diag, a.z, vs, vsi}, a.w, rb, re, sstage, swin);
+        if (a.npoly > 0) {
+            // right preconditioning by the GMRES polynomial: z = p(A) v_k,
+            // then w = A z (gmres.py:181-182)
+            MPK_SYNC_OR_ABORT();   // v_k complete on every CTA
+            poly_apply_dev<T>(A, MPK_POLY_BUFS, reinterpret_cast<const T *>(vk), rb, re, sstage);
+            MPK_SYNC_OR_ABORT();   // z complete
+            an = poly_spmv_dev<T>(A, a.pacc, a.w, rb, re, sstage);
+        } else {
+            an = phase_a_spmv<T>(A, XSlab<T, TV>{src, vk, dv, rb, re, a.diag, a.z, vs, vsi}, a.w, rb, re, sstage,
+                                 swin);
+        }
         MPK_MARK(1);
         __syncthreads();   // w rows of this CTA visible to the other lanes' 16-byte loads
         const int nbk = BIG ? (nc + kRegMaxCols - 1) / kRegMaxCols : 1;   // column blocks
@@ -640,7 +763,15 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
     {
         T acc[C::KP];
         T ext = T(0);
-        if (!BIG) {
+        if (!BIG && a.npoly > 0) {
+            // x = x0 + p(A) (V_k d) (gmres.py:194-196): V_k d into the free
+            // w' slot, then the polynomial, then the update
+            reg_phase<T, kRegCorrect, TV>(Vb, a.ld, k, rb, re, a.n, nullptr, a.wp, sd, acc, ext, nullptr, nullptr,
+                                          (3 * k) & 1, vsi);
+            MPK_SYNC_OR_ABORT();
+            poly_apply_dev<T>(A, MPK_POLY_BUFS, a.wp, rb, re, sstage);
+            for (int64_t r = rb + tid; r < re; r += kFB) a.x_out[r] = RN<T>::add(a.x0[r], a.pacc[r]);
+        } else if (!BIG) {
             reg_phase<T, kRegCorrect, TV>(Vb, a.ld, k, rb, re, a.n, a.x0, a.x_out, sd, acc, ext, nullptr, a.diag,
                                       (3 * k) & 1, vsi);   // after step k-1's phase C (index 3k-1)
         } else {   // big: x += V_b d_b block by block (no diagonal preconditioner here)
@@ -656,6 +787,7 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
     if (a.prof && tid < kProfSlots) g_fused_prof[blockIdx.x * kProfSlots + tid] = s_prof[tid];
 #undef MPK_MARK
 #undef MPK_SYNC_OR_ABORT
+#undef MPK_POLY_BUFS
 }
 
 }  // namespace mpk

@@ -64,22 +64,11 @@ __device__ __forceinline__ void for_rows(const Op &A, X x, T *sb, F &&fn) {
             // neighbours), bit-identical to row(); scalar tail past n - n % R
             const int64_t ng = A.n / R;
             auto xv = [&](int64_t c) { return x.vec(c); };
-            // two groups per thread per trip, both groups' loads in flight
-            // before either is evaluated (fn still sees rows in stride order)
+            // one group per thread per trip: two in flight raised the
+            // standalone kernel to 114 registers (BentPipe's double
+            // coefficient arithmetic) and halved its occupancy
             const int64_t st = gstride();
             int64_t gi = gtid();
-            for (; gi + st < ng; gi += 2 * st) {
-                typename Op::GroupIn in0, in1;
-                A.group_load(gi * R, xv, x, in0);
-                A.group_load((gi + st) * R, xv, x, in1);
-                T o[R];
-                A.group_eval(gi * R, in0, o);
-#pragma unroll
-                for (int e = 0; e < R; ++e) fn(gi * R + e, o[e]);
-                A.group_eval((gi + st) * R, in1, o);
-#pragma unroll
-                for (int e = 0; e < R; ++e) fn((gi + st) * R + e, o[e]);
-            }
             for (; gi < ng; gi += st) {
                 T o[R];
                 A.row_group(gi * R, xv, x, o);
@@ -538,8 +527,11 @@ __global__ void __launch_bounds__(kBlock) k_spmv(Op A, const T *__restrict__ x, 
 // Banded CSR (A.band > 0): chunks of kSpmvChunk rows per CTA, x staged in a
 // shared-memory window per chunk (csr_chunk), K entries per lane in flight.
 constexpr int kSpmvChunk = 1024;
+// (ncu, config 5: K = 16 took 97 / 164 registers and capped occupancy at
+// 25% / 12.5%; the bounds below keep 4 / 3 CTAs per SM)
 template <typename T, int K>
-__global__ void __launch_bounds__(kBlock) k_spmv_win(CsrOp<T> A, const T *__restrict__ x, T *__restrict__ y) {
+__global__ void __launch_bounds__(kBlock, sizeof(T) == 4 ? 4 : 3)
+    k_spmv_win(CsrOp<T> A, const T *__restrict__ x, T *__restrict__ y) {
     extern __shared__ __align__(16) unsigned char dsm_win[];
     __shared__ T sbuf[(kBlock / 32) * kCsrWarpBuf];
     T *sx = reinterpret_cast<T *>(dsm_win);

@@ -45,7 +45,7 @@ from . import device as D
 from .engine import OFF_BN2, OFF_CHANGED, OFF_RN2, OFF_RN2_LOW, CycleWorkspace, Readout, sqrt_in
 
 OFF_TIMEOUT = OFF_RN2 + 20   # int32 set by mpk_comm_reduce_ctl when a cross-rank barrier timed out
-from .errors import DimensionMismatchError, ZeroRightHandSideError
+from .errors import PrecisionMismatchError, DimensionMismatchError, ZeroRightHandSideError
 from .gmres import ConvergenceReport, CycleState, HistoryEntry, SolverConfig, detect_loss_of_accuracy
 from .multiprecision import IrConfig
 from .precision import Precision
@@ -354,6 +354,32 @@ class LocalSystem:
         c.epoch = pb.own["epoch"]
         return c
 
+    def diag_precond(self, M, prec: Precision) -> _lib.MpkPrecond:
+        """mpk_precond of a block-Jacobi(1) right preconditioner (a diagonal
+        scaling, applied inside the row-partitioned cycle kernel): `lu` points
+        at row0 of the GLOBAL diagonal, so the halo rows the SpMV reads
+        (local indices below 0 or past n) find their a_ii as well."""
+        key = ("diag", id(M), prec)
+        got = getattr(self, "_diag_cache", {}).get(key)
+        if got is not None:
+            return got[0]
+        if getattr(M, "kind", None) != "jacobi" or M.data.block_size != 1:
+            raise ValueError("row-partitioned cycles support block Jacobi with 1x1 blocks (or no preconditioner)")
+        if M.precision is not prec or M.n != self.n_global:
+            raise PrecisionMismatchError("preconditioner must be built on the global matrix in the cycle precision")
+        nat = M.native()
+        d = _lib.MpkPrecond()
+        d.kind = _lib.PC_JACOBI
+        d.dtype = prec.code
+        d.n = self.n
+        d.block = 1
+        d.lu = nat.lu + self.r0 * prec.dtype.itemsize
+        d.piv = nat.piv + self.r0 * 4
+        if not hasattr(self, "_diag_cache"):
+            self._diag_cache = {}
+        self._diag_cache[key] = (d, M)
+        return d
+
     def close(self):
         for pb in self._peers.values():
             pb.close()
@@ -392,13 +418,18 @@ class _DistWs:
     def bnorm2(self, b, prec):
         self.ws.bnorm2(b, prec)
 
-    def cycle(self, prec, r0, rnorm2_off, x0, x_out, steps_cap, exit_tol, norm_scale, rule, orth="cgs2"):
+    def cycle(self, prec, r0, rnorm2_off, x0, x_out, steps_cap, exit_tol, norm_scale, rule, orth="cgs2",
+              M=None):
         ws = self.ws
         d = ws.desc
         mat = self.s.op(prec)
         ws._pins = [mat, self._comm_struct]
         d.A = ctypes.pointer(mat)
         d.M = None
+        if M is not None:
+            md = self.s.diag_precond(M, prec)
+            ws._pins.append(md)
+            d.M = ctypes.pointer(md)
         d.dtype = prec.code
         d.m = ws.m
         d.steps_cap = int(steps_cap)
@@ -459,9 +490,11 @@ def _local_vec(sysm: LocalSystem, v, dtype):
 
 
 def dist_gmres_restarted(sysm: LocalSystem, b, x0, cfg: SolverConfig, norm_baseline=None,
-                         explicit_restart_on_loss=True, phase=None):
+                         explicit_restart_on_loss=True, phase=None, M=None):
     """gmres_restarted (reference gmres.py:221-308) on the rank's rows; the
-    report (identical on every rank) carries the rank-local x."""
+    report (identical on every rank) carries the rank-local x.  M: None or a
+    block-Jacobi(1) preconditioner built on the global matrix (right
+    preconditioning, applied inside the cycle kernel)."""
     prec = cfg.precision
     if cfg.m + 1 > 52:
         raise ValueError("row-partitioned cycles support m <= 51")
@@ -495,7 +528,7 @@ def dist_gmres_restarted(sysm: LocalSystem, b, x0, cfg: SolverConfig, norm_basel
         if remaining <= 0 or restarts >= cfg.max_restarts:
             break
         cap = max(1, min(cfg.m, remaining))
-        ws.cycle(prec, r, OFF_RN2, x, x, cap, cfg.rtol, scale, cfg.breakdown_rule, cfg.orthogonalization)
+        ws.cycle(prec, r, OFF_RN2, x, x, cap, cfg.rtol, scale, cfg.breakdown_rule, cfg.orthogonalization, M)
         ws.residual(prec, bd, x, r)
         out = ws.read(rn2_dtype=prec.dtype)
         state = CycleState(out.steps, out.implicit, scale, out.breakdown)
@@ -514,8 +547,9 @@ def dist_gmres_restarted(sysm: LocalSystem, b, x0, cfg: SolverConfig, norm_basel
                              phase_iters={phase: total})
 
 
-def dist_gmres_ir(sysm: LocalSystem, b, x0, cfg: IrConfig):
-    """gmres_ir (reference multiprecision.py:120-233) on the rank's rows."""
+def dist_gmres_ir(sysm: LocalSystem, b, x0, cfg: IrConfig, M=None):
+    """gmres_ir (reference multiprecision.py:120-233) on the rank's rows.
+    M: None or a block-Jacobi(1) preconditioner (fp32, global matrix)."""
     prec, low = cfg.outer_precision, cfg.inner.precision
     if prec is not Precision.binary64 or low is not Precision.binary32:
         raise ValueError("the device refinement runs fp32 inside fp64")
@@ -567,7 +601,7 @@ def dist_gmres_ir(sysm: LocalSystem, b, x0, cfg: IrConfig):
             continue
         cap = max(1, min(cfg.inner.m, remaining))
         ws.cycle(low, r32, OFF_RN2_LOW, zeros32, u32, cap, floor, None, cfg.inner.breakdown_rule,
-                 cfg.inner.orthogonalization)
+                 cfg.inner.orthogonalization, M)
         _lib.check(lib.mpk_ir_update(n, D.ptr(x), D.ptr(u32), ws.ws.at(OFF_CHANGED), D.stream()))
         ws.residual(prec, bd, x, r, r32)
         out = ws.read()

@@ -195,3 +195,34 @@ def test_fp32_restarted_matches_single_gpu(cuda, P):
     for _, xl, (r0, r1) in res:
         x[r0:r1] = xl
     assert np.abs(x - ref.x).max() <= 1e-3 * np.abs(ref.x).max()
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_jacobi1_row_partitioned(cuda, P):
+    """Block-Jacobi(1) right preconditioning inside the row-partitioned cycle
+    (diagonal of the GLOBAL matrix; halo rows scaled by their own a_ii):
+    same report on every rank, counts within a cycle of the one-GPU solve."""
+    A = mk.synthetic_irregular(6000, signs="negative", dominance=1.001, shift=1e-3, far_frac=0.01, band=300)
+    A_low = mk.convert_matrix(A, P32)
+    M64 = mk.build_block_jacobi(A, 1)
+    M32 = mk.build_block_jacobi(A_low, 1)
+    b = np.ones(A.n)
+    inner = mk.SolverConfig(m=50, rtol=1e-4, precision=P32, max_iters=20000, breakdown_rule="u")
+
+    def fn(comm):
+        sysm = dd.LocalSystem(comm, A, A_low)
+        try:
+            r64 = dd.dist_gmres_restarted(sysm, b, np.zeros(A.n), mk.SolverConfig(m=50, rtol=1e-10, max_iters=20000),
+                                          M=M64)
+            rir = dd.dist_gmres_ir(sysm, b, np.zeros(A.n), mk.IrConfig(inner=inner, rtol=1e-10), M=M32)
+            return r64.total_iters, rir.total_iters, rir.converged, rir.final_explicit_relres
+        finally:
+            sysm.close()
+
+    res = dd.run_virtual_ranks(P, fn)
+    assert all(r == res[0] for r in res)
+    it64, itir, conv, rel = res[0]
+    one64 = mk.gmres_restarted(A, M64, b, np.zeros(A.n), mk.SolverConfig(m=50, rtol=1e-10, max_iters=20000))
+    oneir = mk.gmres_ir(A, b, np.zeros(A.n), mk.IrConfig(inner=inner, rtol=1e-10), M=M32, A_low=A_low)
+    assert conv and rel <= 1e-10
+    assert abs(it64 - one64.total_iters) <= 50 and abs(itir - oneir.total_iters) <= 50

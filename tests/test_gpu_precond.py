@@ -205,3 +205,50 @@ def test_device_block_lu_large_batch(cuda):
     ref = O.jacobi_build(A.row_ptr, A.col_idx, A.values, 42, np.float64)
     want = ref(v)
     assert np.abs(got - want).max() <= 1e-10 * np.abs(want).max()
+
+
+@pytest.mark.parametrize("preset,nx,deg", [("UniFlow2D", 64, 25), ("Laplace2D", 32, 10), ("Stretched2D", 32, 20)])
+def test_poly_fused_cycle_matches_multikernel(cuda, preset, nx, deg):
+    """The GMRES polynomial runs inside the persistent cycle kernel (z = p(A) v_k
+    and the correction's p(A)(V_k d) with one grid barrier per SpMV, same
+    per-row roundings as k_poly_*): same counts and histories to rounding as
+    the multi-kernel path (desc flag 4), and within a cycle of the oracle."""
+    from oracle import mpk_oracle as O
+    from paper_2105_07544_b200 import _lib
+    from paper_2105_07544_b200.engine import CycleWorkspace
+
+    A = L(preset, nx)
+    A32 = mk.convert_matrix(A, P.binary32)
+    M32 = mk.build_gmres_poly(A32, deg, np.ones(A.n, np.float32))
+    inner = mk.SolverConfig(m=50, rtol=1e-4, precision=P.binary32, max_iters=3000)
+    cfg = mk.IrConfig(inner=inner, rtol=1e-10)
+    fused = mk.gmres_ir(A, np.ones(A.n), np.zeros(A.n), cfg, M=M32, A_low=A32)
+    assert _lib.last_cycle_kernel() == "k_cycle_reg"
+    ws = CycleWorkspace.get(A.n, 50, P.binary32)
+    ws.flags = 4
+    try:
+        multi = mk.gmres_ir(A, np.ones(A.n), np.zeros(A.n), cfg, M=M32, A_low=A32)
+        assert _lib.last_cycle_kernel() == "multi-kernel"
+    finally:
+        ws.flags = 0
+    assert fused.converged == multi.converged
+    assert abs(fused.total_iters - multi.total_iters) <= 50
+    # the first cycle's implicit residuals agree to rounding (the two paths
+    # reduce the dot products in different orders)
+    def first_cycle(rep):
+        out = []
+        for e in rep.history[1:]:
+            if e.phase != "inner":
+                break
+            out.append(e.implicit_relres)
+        return np.array(out)
+    hf, hm = first_cycle(fused), first_cycle(multi)
+    assert len(hf) == len(hm)
+    assert np.abs(hf / hm - 1).max() <= 1e-4
+    rp, ci, v = O.stencil_csr(preset, nx)
+    d = M32.data
+    ref = O.refine((rp, ci, v), np.ones(A.n), np.zeros(A.n), 50, 1e-10, 3000,
+                   M=O.Poly(d.roots, d.degree, d.requested_degree, d.truncated, rp, ci, v.astype(np.float32)))
+    assert fused.converged == ref.converged
+    if ref.converged:
+        assert abs(fused.total_iters - ref.iters) <= 50
