@@ -12,7 +12,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libmpkb200.so")
+# MPK_LIB_PATH: an alternative build of the same library (A/B measurements)
+LIB_PATH = os.environ.get("MPK_LIB_PATH") or os.path.join(HERE, "_lib", "libmpkb200.so")
 
 F32, F64 = 0, 1
 CSR, STENCIL = 0, 1

@@ -610,18 +610,21 @@ int launch_fused_reg(const Op &op, const mpk_cycle_desc *d, int cap, double tf, 
     constexpr bool half = !std::is_same<T, TV>::value;
     if (multi && big) return fail(MPK_EUNSUPPORTED, "row-partitioned cycles support m <= 51");
     if (half && (multi || big)) return fail(MPK_EUNSUPPORTED, "binary16 basis: one GPU, m <= 51");
+    const bool poly = d->M && d->M->kind == MPK_PC_POLY;
+    if (poly && (half || multi || big)) return fail(MPK_EUNSUPPORTED, "polynomial cycle: one GPU, m <= 51");
     void (*kern)(Op, FusedArgs<T>);
     if constexpr (half) kern = k_cycle_reg<T, Op, false, false, TV>;
-    else kern = multi ? k_cycle_reg<T, Op, false, true>
-                      : (big ? k_cycle_reg<T, Op, true, false> : k_cycle_reg<T, Op, false, false>);
+    else kern = poly ? k_cycle_reg<T, Op, false, false, T, true>
+                     : multi ? k_cycle_reg<T, Op, false, true>
+                             : (big ? k_cycle_reg<T, Op, true, false> : k_cycle_reg<T, Op, false, false>);
     const size_t nslot = big ? (size_t)m + 2 : (size_t)kFSlots;
     int64_t win = 0;   // banded CSR: x window of phase A's SpMV chunks
     if constexpr (!Op::kStencil)
         if (!multi) win = csr_window_elems(op, kRegCsrChunk);
     const size_t smem = sizeof(T) * ((big ? 0 : (size_t)(m + 1) * m) + 2 * m + (m + 1) + 2 * nslot + kFW * kFSlots +
                                      (big ? nslot : 0) + kFW * kCsrWarpBuf + (size_t)win);
-    static size_t attr_set[3] = {0, 0, 0};   // per instantiation (TV is a template parameter)
-    const int vi = multi ? 2 : (big ? 1 : 0);
+    static size_t attr_set[4] = {0, 0, 0, 0};   // per kernel (TV is a template parameter)
+    const int vi = poly ? 3 : multi ? 2 : (big ? 1 : 0);
     if (smem > attr_set[vi]) {
         cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (ea != cudaSuccess) {
@@ -710,7 +713,8 @@ int launch_fused_reg(const Op &op, const mpk_cycle_desc *d, int cap, double tf, 
         g_err = std::string("k_cycle_reg: ") + cudaGetErrorString(e);
         return MPK_ELAUNCH;
     }
-    g_last_cycle = half ? "k_cycle_reg/half" : multi ? "k_cycle_reg/multi" : (big ? "k_cycle_reg/big" : "k_cycle_reg");
+    g_last_cycle = half ? "k_cycle_reg/half"
+                        : poly ? "k_cycle_reg/poly" : multi ? "k_cycle_reg/multi" : (big ? "k_cycle_reg/big" : "k_cycle_reg");
     return check_launch("k_cycle_reg");
 }
 

@@ -296,7 +296,10 @@ __device__ __noinline__ T phase_a_spmv(const Op &A, const XS xs, T *w, int64_t r
         // with one group per trip).  UG = 4 spilled (Laplace3D: 5 packs per
         // group) and cost 18% of the C4 cycle; 2 keeps the loads in registers
         constexpr int R = RegCfg<T>::R;
-        constexpr int UG = 2;
+#ifndef MPK_PHASEA_UG
+#define MPK_PHASEA_UG 2
+#endif
+        constexpr int UG = MPK_PHASEA_UG;
         auto xv = [&](int64_t c) { return xs.vec(c); };
         constexpr int64_t S = (int64_t)kFB * R;
         int64_t r = rb + (int64_t)threadIdx.x * R;
@@ -450,8 +453,12 @@ __device__ __noinline__ T poly_spmv_dev(const Op &A, const T *z, T *w, int64_t r
     return an;
 }
 
-template <typename T, class Op, bool BIG, bool MULTI, typename TV = T>
+template <typename T, class Op, bool BIG, bool MULTI, typename TV = T, bool POLY = false>
 __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
+    // POLY: GMRES-polynomial instantiation (one GPU, m <= 51, TV == T); the
+    // others carry no polynomial code (its call sites cost the streaming
+    // phases registers even when not taken)
+    static_assert(!POLY || (!BIG && !MULTI && sizeof(TV) == sizeof(T)), "polynomial cycle: one GPU, m <= 51");
     using C = RegCfg<T>;
     using IO = VIO<T, TV>;
     // basis storage: T, or binary16 holding v * vs (fp32 cycles, one GPU, m <= 51)
@@ -529,7 +536,7 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
         return;                                    \
     }
 
-    if (tid < a.npoly) s_poly[tid] = a.poly[tid];
+    if (POLY && tid < a.npoly) s_poly[tid] = a.poly[tid];
     // built at the (rare) use sites from the kernel parameters: a struct
     // live across the cycle would cost the streaming phases registers
 #define MPK_POLY_BUFS PolyBufs<T>{s_poly, a.npoly, a.pw0, a.pw1, a.pt, a.pacc, a.bar}
@@ -623,7 +630,7 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
         }
         MPK_MARK(0);
         __syncthreads();
-        if (a.npoly > 0) {
+        if (POLY) {
             // right preconditioning by the GMRES polynomial: z = p(A) v_k,
             // then w = A z (gmres.py:181-182)
             MPK_SYNC_OR_ABORT();   // v_k complete on every CTA
@@ -763,7 +770,7 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
     {
         T acc[C::KP];
         T ext = T(0);
-        if (!BIG && a.npoly > 0) {
+        if (POLY) {
             // x = x0 + p(A) (V_k d) (gmres.py:194-196): V_k d into the free
             // w' slot, then the polynomial, then the update
             reg_phase<T, kRegCorrect, TV>(Vb, a.ld, k, rb, re, a.n, nullptr, a.wp, sd, acc, ext, nullptr, nullptr,
