@@ -194,6 +194,16 @@ __device__ __forceinline__ void reg_phase(const TV *V, int64_t ld, int nc, int64
 #define MPK_REG_U(UU, KK) \
     reg_phase_u<T, TV, MODE, UU, KK>(V, ld, nc, rb, re, n, x, y, coef, acc, ext, cm, diag, rev, vsi)
     static_assert(C::KP == 13, "shape table below assumes 13 columns per part");
+    if constexpr (MODE == kRegUpdateNorm || MODE == kRegCorrect) {
+        // update-only passes keep the round-1 shapes: with the exact-width
+        // shapes stream C measured 19% slower (C2 phase profile, 2136 vs
+        // 1795 us per cycle) while streams A and B gained 5-9%
+        if (ncp * 8 <= C::KP) MPK_REG_U(8, 1);
+        else if (ncp * 4 <= C::KP) MPK_REG_U(4, 3);
+        else if (ncp * 2 <= C::KP) MPK_REG_U(2, 6);
+        else MPK_REG_U(1, 13);
+        return;
+    }
     switch (ncp) {
         case 1: MPK_REG_U(8, 1); break;
         case 2:
@@ -297,7 +307,7 @@ __device__ __noinline__ T phase_a_spmv(const Op &A, const XS xs, T *w, int64_t r
         // group) and cost 18% of the C4 cycle; 2 keeps the loads in registers
         constexpr int R = RegCfg<T>::R;
 #ifndef MPK_PHASEA_UG
-#define MPK_PHASEA_UG 2
+#define MPK_PHASEA_UG 1   // 2 measured 1% slower on C2/C4 (one group's loads suffice with 16 warps)
 #endif
         constexpr int UG = MPK_PHASEA_UG;
         auto xv = [&](int64_t c) { return xs.vec(c); };

@@ -197,6 +197,9 @@ class TorchComm:
                                    % (self.rank, dev, q, pd))
 
     def exchange(self, obj) -> list:
+        from .engine import HOST_STATS
+
+        HOST_STATS["host_collectives"] += 1
         out = [None] * self.size
         self.dist.all_gather_object(out, obj)
         return out

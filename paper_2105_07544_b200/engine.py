@@ -12,6 +12,7 @@ cycle (per refinement for GMRES-IR).
 from __future__ import annotations
 
 import ctypes
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -20,6 +21,10 @@ from . import _lib
 from . import device as D
 from .errors import TriangularBreakdownError
 from .precision import Precision
+
+# optional host-side accounting (tools/dist_check.py): seconds spent waiting
+# in the per-cycle control-block sync, number of reads, host collectives
+HOST_STATS = {"on": False, "sync_s": 0.0, "reads": 0, "host_collectives": 0}
 
 CTL_BYTES = ctypes.sizeof(_lib.MpkCycleCtl)
 OFF_RN2 = (CTL_BYTES + 63) // 64 * 64      # r.r in the cycle dtype (or fp64 outer)
@@ -133,7 +138,13 @@ class CycleWorkspace:
     def read(self, rn2_dtype=np.float64, with_cycle=True) -> Readout:
         """One pinned D2H copy of the control block + stream sync."""
         self.host.copy_(self.ctlbuf, non_blocking=True)
-        D.sync()
+        if HOST_STATS["on"]:
+            t0 = time.perf_counter()
+            D.sync()
+            HOST_STATS["sync_s"] += time.perf_counter() - t0
+            HOST_STATS["reads"] += 1
+        else:
+            D.sync()
         raw = self.host.numpy()
         rn2 = float(np.frombuffer(raw, dtype=rn2_dtype, count=1, offset=OFF_RN2)[0])
         rn2_low = float(np.frombuffer(raw, dtype=np.float32, count=1, offset=OFF_RN2_LOW)[0])

@@ -22,8 +22,17 @@ if share:
 A = mk.generate_stencil(mk.ProblemSpec(sys.argv[1] if len(sys.argv) > 1 else "Laplace2D",
                                        int(sys.argv[2]) if len(sys.argv) > 2 else 32))
 sysm = dd.LocalSystem(comm, A, mk.convert_matrix(A, P.binary32))
-inner = mk.SolverConfig(m=50, rtol=1e-4, precision=P.binary32, max_iters=20000)
+inner = mk.SolverConfig(m=50, rtol=1e-4, precision=P.binary32, max_iters=20000,
+                        breakdown_rule="u" if len(sys.argv) > 3 and sys.argv[3] == "u" else "n_u")
+import time
+from paper_2105_07544_b200.engine import HOST_STATS
+dd.dist_gmres_ir(sysm, np.ones(A.n), np.zeros(A.n), mk.IrConfig(inner=inner, rtol=1e-10))   # warm-up
+HOST_STATS.update(on=True, sync_s=0.0, reads=0, host_collectives=0)
+t0 = time.perf_counter()
 ir = dd.dist_gmres_ir(sysm, np.ones(A.n), np.zeros(A.n), mk.IrConfig(inner=inner, rtol=1e-10))
+wall = time.perf_counter() - t0
+stats = dict(HOST_STATS)
+HOST_STATS["on"] = False
 g64 = dd.dist_gmres_restarted(sysm, np.ones(A.n), np.zeros(A.n), mk.SolverConfig(m=50, rtol=1e-10))
 xs = [None] * comm.size
 dist.all_gather_object(xs, (sysm.r0, g64.x.cpu().numpy()))
@@ -32,7 +41,10 @@ if comm.rank == 0:
     for r0, xl in xs:
         x[r0:r0 + xl.size] = xl
     ref = mk.gmres_restarted(A, None, np.ones(A.n), np.zeros(A.n), mk.SolverConfig(m=50, rtol=1e-10))
-    print(json.dumps({"ir_iters": ir.total_iters, "ir_converged": ir.converged, "ir_relres": ir.final_explicit_relres,
+    print(json.dumps({"ir_wall_s": wall, "ir_refinements": ir.restarts,
+                      "host_s_per_refinement_excl_sync": (wall - stats["sync_s"]) / max(stats["reads"], 1),
+                      "host_collectives_during_solve": stats["host_collectives"], "reads": stats["reads"],
+                      "ir_iters": ir.total_iters, "ir_converged": ir.converged, "ir_relres": ir.final_explicit_relres,
                       "fp64_iters": g64.total_iters, "fp64_converged": g64.converged,
                       "single_fp64_iters": ref.total_iters,
                       "x_maxdiff": float(np.abs(x - ref.x).max() / np.abs(ref.x).max())}), flush=True)
