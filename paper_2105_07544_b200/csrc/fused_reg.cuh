@@ -801,7 +801,12 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
         }
     }
     MPK_MARK(13);
-    if (a.prof && tid < kProfSlots) g_fused_prof[blockIdx.x * kProfSlots + tid] = s_prof[tid];
+    if (a.prof && tid < kProfSlots) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        // slot 15: the SM this CTA ran on (tools/cta_balance.py)
+        g_fused_prof[blockIdx.x * kProfSlots + tid] = (tid == kProfSlots - 1) ? (unsigned long long)smid : s_prof[tid];
+    }
 #undef MPK_MARK
 #undef MPK_SYNC_OR_ABORT
 #undef MPK_POLY_BUFS

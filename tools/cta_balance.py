@@ -25,7 +25,9 @@ for rep in range(3):
     nct = 148
     buf = (ctypes.c_uint64 * (nct * 16))()
     _lib.check(_lib.load().mpk_fused_prof_read(buf, nct))
-    p = np.array(buf[:], dtype=np.float64).reshape(nct, 16) / 1965.0
+    raw = np.array(buf[:], dtype=np.float64).reshape(nct, 16)
+    p = raw / 1965.0
+    p[:, 15] = raw[:, 15]   # smid
     runs.append(p)
 for p in runs:
     streams = p[:, 2] + p[:, 5] + p[:, 8] + p[:, 1]
@@ -36,4 +38,7 @@ s = [p[:, 2] + p[:, 5] + p[:, 8] + p[:, 1] for p in runs]
 print("corr run0-run1 %.3f run1-run2 %.3f" % (np.corrcoef(s[0], s[1])[0, 1], np.corrcoef(s[1], s[2])[0, 1]))
 order = np.argsort(-s[0])
 print("slowest CTAs run0:", order[:12].tolist(), "their run1 rank:", [int((s[1] > s[1][i]).sum()) for i in order[:12]])
+print("smid of the slowest CTAs (run0, run1):", [int(runs[0][i, 15]) for i in order[:12]],
+      [int(runs[1][i, 15]) for i in order[:12]])
 print("per-CTA stream us (run0):", np.round(s[0]).astype(int).tolist())
+print("per-CTA smid (run0):", runs[0][:, 15].astype(int).tolist())
