@@ -618,11 +618,11 @@ int launch_fused_reg(const Op &op, const mpk_cycle_desc *d, int cap, double tf, 
                      : multi ? k_cycle_reg<T, Op, false, true>
                              : (big ? k_cycle_reg<T, Op, true, false> : k_cycle_reg<T, Op, false, false>);
     const size_t nslot = big ? (size_t)m + 2 : (size_t)kFSlots;
-    int64_t win = 0;   // banded CSR: x window of phase A's SpMV chunks
-    if constexpr (!Op::kStencil)
-        if (!multi) win = csr_window_elems(op, kRegCsrChunk);
+    // (banded CSR: staging x in a shared-memory window for phase A's SpMV,
+    // as k_spmv_win does, measured slower inside the cycle -- C5 IR 0.774 vs
+    // 0.690 s, profiles/r02_C5_window_ab.txt -- so the cycle gathers via L1)
     const size_t smem = sizeof(T) * ((big ? 0 : (size_t)(m + 1) * m) + 2 * m + (m + 1) + 2 * nslot + kFW * kFSlots +
-                                     (big ? nslot : 0) + kFW * kCsrWarpBuf + (size_t)win);
+                                     (big ? nslot : 0) + kFW * kCsrWarpBuf);
     static size_t attr_set[4] = {0, 0, 0, 0};   // per kernel (TV is a template parameter)
     const int vi = poly ? 3 : multi ? 2 : (big ? 1 : 0);
     if (smem > attr_set[vi]) {
@@ -664,7 +664,6 @@ int launch_fused_reg(const Op &op, const mpk_cycle_desc *d, int cap, double tf, 
     fa.prof = (d->flags & 8) ? 1 : 0;
     fa.diag = nullptr;
     fa.z = w + 3 * d->ld;
-    fa.csr_win = win > 0 ? 1 : 0;
     if (d->M && d->M->kind == MPK_PC_POLY) {
         // units of the product form with the multi-kernel path's host
         // arithmetic (apply_precond_t): inv = 1/re; tr = 2 re, m2 = re^2 + im^2

@@ -70,7 +70,6 @@ template <typename T> struct FusedArgs {
     CommArgs<T> cm;   // nranks > 1: row-partitioned cycle
     const T *diag;    // k_cycle_reg: diagonal right preconditioner a_ii (block Jacobi k = 1), or nullptr
     T *z;             // k_cycle_reg: z = v_k / a_ii for the CTA's own rows
-    int csr_win = 0;  // k_cycle_reg: banded CSR, x window after the staging buffers (1024 + 2*band elements)
     T vs = T(1), vsi = T(1);   // k_cycle_reg, binary16 basis: stored = v * vs (power of two), vsi = 1 / vs
     // k_cycle_reg with a GMRES-polynomial right preconditioner (npoly > 0):
     // z = p(A) v_k and the correction's p(A) (V_k d) evaluated in-kernel,

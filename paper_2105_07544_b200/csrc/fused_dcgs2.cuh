@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_dcgs2(Op A, FusedArgs<T> a) {
             if (a.diag) a.z[r] = RN<T>::div(v, __ldg(a.diag + r));   // M q_0 on the own rows
         }
         __syncthreads();
-        phase_a_spmv<T>(A, XSlab<T>{src, q0, gm, rb, re, a.diag, a.z}, z, rb, re, sstage, (T *)nullptr);
+        phase_a_spmv<T>(A, XSlab<T>{src, q0, gm, rb, re, a.diag, a.z}, z, rb, re, sstage);
         __syncthreads();
 #pragma unroll
         for (int i = 0; i < C::KP; ++i) a0[i] = T(0);

@@ -265,28 +265,10 @@ __device__ __forceinline__ void reg_write_partials(T (&acc)[RegCfg<T>::KP], int 
 // ||w||^2.  Out of line (noinline) so its register needs (BentPipe
 // coefficient arithmetic, the CSR staging) do not raise register pressure in
 // the streaming phases, which are kept spill-free.
-constexpr int kRegCsrChunk = 1024;   // rows per x-window chunk of a banded CSR SpMV (phase A)
-
 template <typename T, class Op, class XS>
-__device__ __noinline__ T phase_a_spmv(const Op &A, const XS xs, T *w, int64_t rb, int64_t re, T *sstage,
-                                       T *swin) {
+__device__ __noinline__ T phase_a_spmv(const Op &A, const XS xs, T *w, int64_t rb, int64_t re, T *sstage) {
     T an = T(0);
     if constexpr (!Op::kStencil) {
-        if (swin != nullptr) {
-            // banded rows: x of each 1024-row chunk (+- band) staged in shared memory
-            T *sb = sstage + (threadIdx.x >> 5) * kCsrWarpBuf;
-            const bool wide = sizeof(T) == 4 && A.rp[A.n] > 16 * (int64_t)A.n;
-            for (int64_t R = rb; R < re; R += kRegCsrChunk) {
-                const int64_t Re = R + kRegCsrChunk < re ? R + kRegCsrChunk : re;
-                auto put = [&](int64_t r, T wr) {
-                    w[r] = wr;
-                    an += wr * wr;
-                };
-                if (wide) csr_chunk<16>(A, xs, R, Re, swin, sb, put);
-                else csr_chunk<8>(A, xs, R, Re, swin, sb, put);
-            }
-            return an;
-        }
         // CSR: warp-cooperative 32-row groups (coalesced entries, row-sequential sums)
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         T *sb = sstage + warp * kCsrWarpBuf;
@@ -491,7 +473,6 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
     T *sred = sc2 + nslot;                     // kFW * kFSlots
     T *sctmp = sred + kFW * kFSlots;           // big: nslot (the column being rotated)
     T *sstage = sctmp + (big ? nslot : 0);     // kFW * kCsrWarpBuf (CSR SpMV staging)
-    T *swin = a.csr_win ? sstage + kFW * kCsrWarpBuf : nullptr;   // banded CSR x window
     const int xslot = big ? m + 1 : kFExtra;   // partial slot of the extra scalar
     __shared__ T s_gamma, s_beta, s_bn2;
     __shared__ PolyUnit<T> s_poly[kMaxPolyUnits];
@@ -648,8 +629,7 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
             MPK_SYNC_OR_ABORT();   // z complete
             an = poly_spmv_dev<T>(A, a.pacc, a.w, rb, re, sstage);
         } else {
-            an = phase_a_spmv<T>(A, XSlab<T, TV>{src, vk, dv, rb, re, a.diag, a.z, vs, vsi}, a.w, rb, re, sstage,
-                                 swin);
+            an = phase_a_spmv<T>(A, XSlab<T, TV>{src, vk, dv, rb, re, a.diag, a.z, vs, vsi}, a.w, rb, re, sstage);
         }
         MPK_MARK(1);
         __syncthreads();   // w rows of this CTA visible to the other lanes' 16-byte loads
