@@ -1022,6 +1022,15 @@ int mpk_spmv(const mpk_matrix *A, const void *x, void *y, void *stream) {
             using Op = decltype(op);
             if (op.n == 0) return MPK_OK;
             if constexpr (!Op::kStencil) {
+                // row split chosen by row-length statistics (north_star (1)):
+                // short rows thread per row, long banded rows warp-cooperative
+                // with an x window, other long rows warp-cooperative
+                if (A->nnz <= 8 * A->n) {
+                    auto kr = k_spmv_rows<T>;
+                    int g = grid_for(kr, 0, (op.n + 1) / 2);
+                    kr<<<g, kBlock, 0, s>>>(op, (const T *)x, (T *)y);
+                    return check_launch("k_spmv_rows");
+                }
                 const int64_t we = csr_window_elems(op, kSpmvChunk);
                 if (we > 0) {
                     // banded rows: x window in shared memory; 16 entries per

@@ -524,6 +524,24 @@ __global__ void __launch_bounds__(kBlock) k_spmv(Op A, const T *__restrict__ x, 
     for_rows<T>(A, XPlain<T>{x}, sb, [&](int64_t r, T yr) { y[r] = yr; });
 }
 
+// Short CSR rows (<= 8 stored entries on average, e.g. the stencils in CSR
+// form): thread per row.  A warp's 32 rows cover one contiguous run of
+// entries, so each of a row's entry loads is coalesced across the warp and
+// its x gathers hit L1; no shared-memory staging.  Two rows per thread
+// keep two rows' loads in flight.  Same row sums as row() (csr_matvec).
+template <typename T>
+__global__ void __launch_bounds__(kBlock) k_spmv_rows(CsrOp<T> A, const T *__restrict__ x, T *__restrict__ y) {
+    const XPlain<T> xs{x};
+    const int64_t st = gstride();
+    int64_t r = gtid();
+    for (; r + st < A.n; r += 2 * st) {
+        const T y0 = A.row(r, xs), y1 = A.row(r + st, xs);
+        y[r] = y0;
+        y[r + st] = y1;
+    }
+    for (; r < A.n; r += st) y[r] = A.row(r, xs);
+}
+
 // Banded CSR (A.band > 0): chunks of kSpmvChunk rows per CTA, x staged in a
 // shared-memory window per chunk (csr_chunk), K entries per lane in flight.
 constexpr int kSpmvChunk = 1024;
