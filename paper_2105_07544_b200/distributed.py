@@ -357,6 +357,32 @@ class LocalSystem:
         c.epoch = pb.own["epoch"]
         return c
 
+    def prepare(self, precs, m: int, M=None, cycle_prec: Precision | None = None):
+        """Create every device resource a solve needs BEFORE its first
+        cross-rank kernel: peer buffers of each precision set (cudaMalloc +
+        CUDA-IPC open), the cycle workspace, the preconditioner descriptor.
+        Allocation / IPC mapping can wait for the device to go idle, and a
+        peer's persistent kernel spinning at the cross-rank barrier never
+        does, so a rank that allocates lazily while its peers spin
+        deadlocks until the barrier's 20 s timeout.  The first call per
+        resource set ends with one host barrier (every rank is ready); later
+        solves on the same system do no host collective."""
+        key = (tuple(sorted(p.value for p in precs)), m, id(M) if M is not None else None, cycle_prec)
+        done = getattr(self, "_prepared", set())
+        if key in done:
+            return
+        for p in precs:
+            self.peers(p)
+        if cycle_prec is not None:
+            self.workspace(m, cycle_prec)
+            self.comm_struct(cycle_prec)
+            if M is not None:
+                self.diag_precond(M, cycle_prec)
+        D.sync()
+        self.comm.exchange(None)
+        done.add(key)
+        self._prepared = done
+
     def diag_precond(self, M, prec: Precision) -> _lib.MpkPrecond:
         """mpk_precond of a block-Jacobi(1) right preconditioner (a diagonal
         scaling, applied inside the row-partitioned cycle kernel): `lu` points
@@ -504,10 +530,11 @@ def dist_gmres_restarted(sysm: LocalSystem, b, x0, cfg: SolverConfig, norm_basel
     if cfg.basis_precision != "working":
         raise ValueError("row-partitioned cycles keep the basis in the working precision")
     t = D.torch()
-    ws = _DistWs(sysm, cfg.m, prec)
     bd = _local_vec(sysm, b, prec.torch_dtype)
     x = _local_vec(sysm, x0, prec.torch_dtype)
     r = D.empty(sysm.n, prec.torch_dtype)
+    sysm.prepare([prec], cfg.m, M, prec)   # after every allocation of this solve
+    ws = _DistWs(sysm, cfg.m, prec)
     if phase is None:
         phase = "double" if prec is Precision.binary64 else "single"
     ws.bnorm2(bd, prec)
@@ -562,13 +589,14 @@ def dist_gmres_ir(sysm: LocalSystem, b, x0, cfg: IrConfig, M=None):
         raise ValueError("row-partitioned cycles keep the basis in the working precision")
     t = D.torch()
     n = sysm.n
-    ws = _DistWs(sysm, cfg.inner.m, low)
     bd = _local_vec(sysm, b, t.float64)
     x = _local_vec(sysm, x0, t.float64)
     r = D.empty(n, t.float64)
     r32 = D.empty(n, t.float32)
     u32 = D.empty(n, t.float32)
     zeros32 = D.zeros(n, t.float32)
+    sysm.prepare([prec, low], cfg.inner.m, M, low)   # after every allocation of this solve
+    ws = _DistWs(sysm, cfg.inner.m, low)
     ws.bnorm2(bd, prec)
     ws.residual(prec, bd, x, r, r32)
     first = ws.read(with_cycle=False)
