@@ -10,6 +10,8 @@ CASE is one of
   c4_fp64      Laplace3D 200^3,   fp64 GMRES(50), rtol 1e-10
   c4_ir_u      Laplace3D 200^3,   GMRES-IR(50) fp32 inner, breakdown rule "u"
                                   (reference cgs2_append body with u*||w||)
+  c4_fd_u      Laplace3D 200^3,   GMRES-FD(50), fp32 for 2000 iterations then fp64,
+                                  breakdown rule "u" in both phases
   c1_fp64 / c1_ir   Laplace3D 40^3 (quick; used to check the thread spread)
 
 Writes tests/golden/big/<CASE>_t<T>.npz with the counts, flags and the history
@@ -75,7 +77,15 @@ def main():
     else:
         A = mk.generate_stencil(mk.ProblemSpec("Laplace3D", 40))
     b = np.ones(A.n)
-    if case.endswith("fp64"):
+    if "_fd" in case:
+        low = mk.SolverConfig(m=50, rtol=1e-10, precision=P.binary32, max_iters=100000)
+        high = mk.SolverConfig(m=50, rtol=1e-10, max_iters=100000)
+        cfg = mk.FdConfig(switch_iter=2000, low=low, high=high)
+        run = lambda: mk.gmres_fd(A, b, np.zeros(A.n), cfg)  # noqa: E731
+        if case.endswith("_u"):
+            run0 = run
+            run = lambda: with_rule_u(run0)  # noqa: E731
+    elif case.endswith("fp64"):
         cfg = mk.SolverConfig(m=50, rtol=1e-10, max_iters=100000)
         run = lambda: mk.gmres_restarted(A, None, b, np.zeros(A.n), cfg)  # noqa: E731
     else:

@@ -23,6 +23,12 @@ for m in ms:
     t_64, r_64 = timed(lambda: mk.gmres_restarted(A, None, b, x0, mk.SolverConfig(m=m, rtol=1e-10, max_iters=100000)))
     row = {"m": m, "fp64_s": t_64, "fp64_iters": r_64.total_iters, "ir_s": t_ir, "ir_iters": r_ir.total_iters,
            "speedup": t_64 / t_ir, "converged": bool(r_ir.converged and r_64.converged)}
+    if m <= 51:   # third precision: binary16 Krylov basis in the inner cycles
+        inner16 = mk.SolverConfig(m=m, rtol=1e-4, precision=P.binary32, max_iters=100000,
+                                  basis_precision="binary16")
+        t_h, r_h = timed(lambda: mk.gmres_ir(A, b, x0, mk.IrConfig(inner=inner16, rtol=1e-10), A_low=Al))
+        row.update(ir16_s=t_h, ir16_iters=r_h.total_iters, ir16_speedup=t_64 / t_h,
+                   ir16_converged=bool(r_h.converged))
     out.append(row)
     print(json.dumps(row), flush=True)
 print(json.dumps({"sweep": "BentPipe2D 1500^2, b = ones, rtol 1e-10, one B200", "rows": out}))
