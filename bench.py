@@ -464,6 +464,13 @@ def main():
                                      "final_relres": repsirh[-1].final_explicit_relres,
                                      "speedup_vs_fp32_basis_ir": (ms_ir / args.steps) / (msirh / args.steps),
                                      "ir_speedup_vs_fp64": ms64 / (msirh / args.steps)}
+            icfgb = dataclasses.replace(icfg, inner=dataclasses.replace(inner, basis_precision="bfloat16"))
+            solve_irb = lambda: mk.gmres_ir(A, b_dev, x0_dev, icfgb, M=M32, A_low=A_low)  # noqa: E731
+            solve_irb()
+            msirb, repsirb = timed(solve_irb, 1)
+            out["bfloat16_basis"] = {"ir_s": msirb / 1e3, "ir_iters": repsirb[-1].total_iters,
+                                     "ir_converged": bool(repsirb[-1].converged),
+                                     "ir_speedup_vs_fp64": ms64 / msirb}
     note("fp64 done")
     if not args.no_e2e:
         # public API with host (pinned) inputs; every step copies b and x0 in

@@ -251,7 +251,8 @@ typedef struct mpk_cycle_desc {
                                bit4: lagged one-reduction CGS2 (identity preconditioner, m <= 51);
                                bit5: basis stored in binary16 (scaled by a power of two; binary32
                                      cycles, one GPU, m <= 51, CGS2, identity or Jacobi(1)); V then
-                                     holds ld * (m + 1) binary16 values */
+                                     holds ld * (m + 1) binary16 values;
+                               bit6: the same with bfloat16 basis storage */
     const mpk_comm *comm;   /* nranks > 1: this rank's view of the communicator */
 } mpk_cycle_desc;
 

@@ -441,9 +441,19 @@ def round16(v, s):
     return ((v * np.float32(s)).astype(np.float16).astype(np.float32) / np.float32(s)).astype(v.dtype)
 
 
+def round_bf16(v, s):
+    """Stored value of a bfloat16 basis entry (round to nearest even on the
+    upper 16 bits of the float32 v*s), read back as v' = bf16/s."""
+    f = (v * np.float32(s)).astype(np.float32)
+    u = f.view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
+    return ((r.astype(np.uint32).view(np.float32)) / np.float32(s)).astype(v.dtype)
+
+
 def one_cycle(A, M, b, x0, m, tol, r0=None, scale=None, cap=None, rule="n_u", basis16=False):
     """gmres_cycle (gmres.py:134-205). A = (rp, ci, vals); M callable or None.
-    basis16: store the basis columns rounded to binary16 (round16)."""
+    basis16: store the basis columns rounded to binary16 (True / "binary16",
+    round16) or bfloat16 ("bfloat16", round_bf16)."""
     rp, ci, vals = A
     dt = vals.dtype
     Mf = M if M is not None else (lambda v: v)
@@ -458,7 +468,8 @@ def one_cycle(A, M, b, x0, m, tol, r0=None, scale=None, cap=None, rule="n_u", ba
     n = b.shape[0]
     s16 = basis16_scale(n)
     V = np.zeros((n, steps_cap + 1), dtype=dt, order="F")
-    V[:, 0] = round16(r / gam, s16) if basis16 else r / gam
+    rnd = (lambda v: round_bf16(v, s16)) if basis16 == "bfloat16" else (lambda v: round16(v, s16))
+    V[:, 0] = rnd(r / gam) if basis16 else r / gam
     cnt = 1
     lsq = RotatedLsq(steps_cap, gam, sc, dt)
     rels = []
@@ -468,7 +479,7 @@ def one_cycle(A, M, b, x0, m, tol, r0=None, scale=None, cap=None, rule="n_u", ba
         w = spmv_seq(rp, ci, vals, Mf(V[:, k]))
         coeffs, beta, ok, q = cgs2_step(V, cnt, w, rule)
         if ok:
-            V[:, cnt] = round16(q, s16) if basis16 else q
+            V[:, cnt] = rnd(q) if basis16 else q
             cnt += 1
         rel = lsq.push(coeffs, beta)
         rels.append(rel)

@@ -712,7 +712,7 @@ int launch_fused_reg(const Op &op, const mpk_cycle_desc *d, int cap, double tf, 
         g_err = std::string("k_cycle_reg: ") + cudaGetErrorString(e);
         return MPK_ELAUNCH;
     }
-    g_last_cycle = half ? "k_cycle_reg/half"
+    g_last_cycle = half ? (std::is_same<TV, __half>::value ? "k_cycle_reg/half" : "k_cycle_reg/bf16")
                         : poly ? "k_cycle_reg/poly" : multi ? "k_cycle_reg/multi" : (big ? "k_cycle_reg/big" : "k_cycle_reg");
     return check_launch("k_cycle_reg");
 }
@@ -819,19 +819,22 @@ template <typename T> int run_cycle(const mpk_cycle_desc *d, cudaStream_t s) {
     // register kernel applies it inside its SpMV input and correction
     const bool diag1 = precond && d->M->kind == MPK_PC_JACOBI && d->M->block == 1 && d->M->n == n &&
                        d->M->dtype == d->dtype;
-    if (d->flags & 32) {
-        // binary16 basis storage (SolverConfig.basis_precision = "binary16")
+    if (d->flags & (32 | 64)) {
+        // 16-bit basis storage (SolverConfig.basis_precision = "binary16" /
+        // "bfloat16")
         if constexpr (sizeof(T) == 4) {
             const bool ok = (!precond || diag1) && !(d->flags & 16) && !(d->flags & 4) && d->nranks <= 1 &&
                             m + 1 <= kRegMaxCols && (uintptr_t)d->x_out % 16 == 0 && (uintptr_t)d->V % 16 == 0 &&
-                            (uintptr_t)d->work % 16 == 0 && (uintptr_t)d->r0 % 16 == 0;
+                            (uintptr_t)d->work % 16 == 0 && (uintptr_t)d->r0 % 16 == 0 &&
+                            (d->flags & (32 | 64)) != (32 | 64);
             if (!ok)
-                return fail(MPK_EUNSUPPORTED, "binary16 basis: one GPU, m <= 51, CGS2, identity or Jacobi(1)");
+                return fail(MPK_EUNSUPPORTED, "16-bit basis: one GPU, m <= 51, CGS2, identity or Jacobi(1)");
             return with_op<T>(d->A, [&](auto op) -> int {
+                if (d->flags & 64) return launch_fused_reg<T, decltype(op), __nv_bfloat16>(op, d, cap, tf, u, s);
                 return launch_fused_reg<T, decltype(op), __half>(op, d, cap, tf, u, s);
             });
         } else {
-            return fail(MPK_EUNSUPPORTED, "binary16 basis storage needs binary32 cycles");
+            return fail(MPK_EUNSUPPORTED, "16-bit basis storage needs binary32 cycles");
         }
     }
     if ((d->flags & 16) && (!precond || (diag1 && d->nranks <= 1)) && m + 1 <= kRegMaxCols &&

@@ -7,10 +7,13 @@
 // and sqrt are IEEE round-to-nearest and fp32 subnormals are preserved.
 #pragma once
 
+#include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string.h>
+
+#include <type_traits>
 
 #include "../../include/mpk_b200.h"
 
@@ -79,6 +82,16 @@ __device__ __forceinline__ Pack<__half> ldcg16(const __half *p) {
     return r;
 }
 
+__device__ __forceinline__ Pack<__nv_bfloat16> ldcg16(const __nv_bfloat16 *p) {
+    Pack<__nv_bfloat16> r;
+    uint32_t w[4];
+    asm volatile("ld.global.cg.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                 : "l"(p));
+    memcpy(&r, w, 16);
+    return r;
+}
+
 // Basis element I/O: V stored in TV, arithmetic in T.  For TV == T the
 // value itself; binary16 stores v*s and reads back h*(1/s) with s a power of
 // two (exact scaling: it only moves the normalised basis entries, ~1/sqrt(n),
@@ -91,6 +104,12 @@ template <> struct VIO<float, __half> {
     static __device__ __forceinline__ float get(__half v, float si) { return __fmul_rn(__half2float(v), si); }
     static __device__ __forceinline__ __half put(float v, float s) { return __float2half_rn(__fmul_rn(v, s)); }
 };
+// bfloat16 (8-bit significand, fp32's exponent range): the same power-of-two
+// scaling is kept for uniformity (exact, and harmless to the range)
+template <> struct VIO<float, __nv_bfloat16> {
+    static __device__ __forceinline__ float get(__nv_bfloat16 v, float si) { return __fmul_rn(__bfloat162float(v), si); }
+    static __device__ __forceinline__ __nv_bfloat16 put(float v, float s) { return __float2bfloat16_rn(__fmul_rn(v, s)); }
+};
 
 // Raw (unscaled) values of a 16-byte basis group as T: the binary16 stream
 // kernels fold the power-of-two scale into their coefficients / partial sums
@@ -100,11 +119,19 @@ __device__ __forceinline__ void raw_vals(const Pack<TV> &p, T (&o)[16 / sizeof(T
     if constexpr (sizeof(TV) == sizeof(T)) {
 #pragma unroll
         for (int e = 0; e < (int)(16 / sizeof(TV)); ++e) o[e] = p.v[e];
-    } else {
+    } else if constexpr (std::is_same<TV, __half>::value) {
         const __half2 *h = reinterpret_cast<const __half2 *>(p.v);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const float2 f = __half22float2(h[q]);
+            o[2 * q] = f.x;
+            o[2 * q + 1] = f.y;
+        }
+    } else {
+        const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(p.v);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float2 f = __bfloat1622float2(h[q]);
             o[2 * q] = f.x;
             o[2 * q + 1] = f.y;
         }

@@ -346,14 +346,13 @@ template <typename T, typename TV> __device__ __forceinline__ Pack<T> ldv(const 
     if constexpr (sizeof(TV) == sizeof(T)) {
         return ldcg16(p);
     } else {
-        static_assert(sizeof(T) == 4 && sizeof(TV) == 2, "binary16 basis with fp32 arithmetic");
+        static_assert(sizeof(T) == 4 && sizeof(TV) == 2, "16-bit basis with fp32 arithmetic");
         const uint2 w = __ldcg(reinterpret_cast<const uint2 *>(p));
-        const __half2 h0 = *reinterpret_cast<const __half2 *>(&w.x), h1 = *reinterpret_cast<const __half2 *>(&w.y);
+        TV h[4];
+        memcpy(h, &w, 8);
         Pack<T> q;
-        q.v[0] = VIO<T, TV>::get(__low2half(h0), vsi);
-        q.v[1] = VIO<T, TV>::get(__high2half(h0), vsi);
-        q.v[2] = VIO<T, TV>::get(__low2half(h1), vsi);
-        q.v[3] = VIO<T, TV>::get(__high2half(h1), vsi);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) q.v[e] = VIO<T, TV>::get(h[e], vsi);
         return q;
     }
 }
@@ -361,11 +360,11 @@ template <typename T, typename TV> __device__ __forceinline__ void stv(TV *p, co
     if constexpr (sizeof(TV) == sizeof(T)) {
         stcg16(p, q);
     } else {
-        const __half2 h0 = __halves2half2(VIO<T, TV>::put(q.v[0], vs), VIO<T, TV>::put(q.v[1], vs));
-        const __half2 h1 = __halves2half2(VIO<T, TV>::put(q.v[2], vs), VIO<T, TV>::put(q.v[3], vs));
+        TV h[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) h[e] = VIO<T, TV>::put(q.v[e], vs);
         uint2 w;
-        w.x = *reinterpret_cast<const uint32_t *>(&h0);
-        w.y = *reinterpret_cast<const uint32_t *>(&h1);
+        memcpy(&w, h, 8);
         __stcg(reinterpret_cast<uint2 *>(p), w);
     }
 }

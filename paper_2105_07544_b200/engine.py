@@ -57,7 +57,8 @@ class CycleWorkspace:
         # zero-initialised: rows [n, ld) of every column stay zero (the fused
         # kernel's 16-byte row groups and chunk tails read them).  A binary16
         # basis (SolverConfig.basis_precision) halves its bytes.
-        self.V = t.zeros((self.m + 1) * self.ld, dtype=t.float16 if basis == "binary16" else td, device=dev)
+        vdt = {"binary16": t.float16, "bfloat16": t.bfloat16}.get(basis, td)
+        self.V = t.zeros((self.m + 1) * self.ld, dtype=vdt, device=dev)
         # + 512 elements: 1-D bulk copies of a 256-row tile may run past w''s ld
         self.work = t.zeros(4 * self.ld + 512, dtype=td, device=dev)
         self.hess = t.zeros(int(lib.mpk_cycle_hess_bytes(self.m, prec.code)), dtype=t.uint8, device=dev)
@@ -131,7 +132,7 @@ class CycleWorkspace:
         d.nranks = 1
         if basis != self.basis:
             raise ValueError("workspace holds a %s basis, cycle asked for %s" % (self.basis, basis))
-        d.flags = self.flags | (16 if orth == "dcgs2" else 0) | (32 if basis == "binary16" else 0)
+        d.flags = self.flags | (16 if orth == "dcgs2" else 0) | {"binary16": 32, "bfloat16": 64}.get(basis, 0)
         _lib.check(D.lib().mpk_cycle_run(ctypes.byref(d), D.stream()))
 
     # -- readback -----------------------------------------------------------

@@ -22,14 +22,16 @@ def ir(A, basis, m=50, rule="n_u", M=None, max_iters=20000):
     return mk.gmres_ir(A, np.ones(A.n), np.zeros(A.n), mk.IrConfig(inner=inner, rtol=1e-10), M=M)
 
 
+@pytest.mark.parametrize("basis", ["binary16", "bfloat16"])
 @pytest.mark.parametrize("preset,nx", [("Laplace3D", 20), ("Laplace2D", 48), ("BentPipe2D", 64),
                                        ("UniFlow2D", 24)])
-def test_binary16_basis_ir_vs_oracle(cuda, preset, nx):
+def test_binary16_basis_ir_vs_oracle(cuda, preset, nx, basis):
     A = mk.generate_stencil(mk.ProblemSpec(preset, nx))
-    rep = ir(A, "binary16")
-    assert _lib.last_cycle_kernel() == "k_cycle_reg/half"
+    rep = ir(A, basis)
+    assert _lib.last_cycle_kernel() == ("k_cycle_reg/half" if basis == "binary16" else "k_cycle_reg/bf16")
     rp, ci, v = O.stencil_csr(preset, nx)
-    ref = O.refine((rp, ci, v), np.ones(A.n), np.zeros(A.n), 50, 1e-10, 20000, basis16=True)
+    ref = O.refine((rp, ci, v), np.ones(A.n), np.zeros(A.n), 50, 1e-10, 20000,
+                   basis16=True if basis == "binary16" else "bfloat16")
     assert rep.converged and ref.converged and rep.final_explicit_relres <= 1e-10
     assert abs(rep.total_iters - ref.iters) <= 50, (rep.total_iters, ref.iters)
     # per-refinement explicit residuals track the oracle's (fp16 rounding of

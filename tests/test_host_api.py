@@ -136,4 +136,6 @@ def test_binary16_basis_validation():
     with pytest.raises(ValueError):
         mk.SolverConfig(precision=mk.Precision.binary32, orthogonalization="dcgs2", basis_precision="binary16")
     with pytest.raises(ValueError):
-        mk.SolverConfig(basis_precision="bfloat16")
+        mk.SolverConfig(basis_precision="float8")
+    with pytest.raises(ValueError):
+        mk.SolverConfig(precision=mk.Precision.binary64, basis_precision="bfloat16")
