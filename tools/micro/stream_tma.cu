@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(NT, 1) k_reg(const float *V, int64_t ld, int n
 // consumer warp t % 16, buffer (t / 16) & 1; lane = row (U rows per lane).
 // The producer warp issues tiles in order, waiting on the target buffer's
 // empty barrier (1 arrival: the consumer warp's lane 0).
-constexpr int kTileB = 7 * 1024;        // bytes per buffer (2 per warp: 224 KB)
+constexpr int kTileB = 6656;            // bytes per buffer (2 per warp: 208 KB)
 template <int U, int NCMAX>
 __global__ void __launch_bounds__(NT + 32, 1) k_tma(const __grid_constant__ CUtensorMap tmap, int64_t ld, int nc,
                                                      int64_t n, const float *x, float *y, const float *coef,
@@ -222,7 +222,7 @@ int main() {
         cudaEventCreate(&b);
         for (int nc : {4, 8, 13, 16, 20, 26, 32, 40, 51}) {
             const int ncp = (nc + 3) / 4;
-            // rows per tile: the largest 32*U with (nc + 1) * 32U * 4 <= 7 KB
+            // rows per tile: the largest 32*U with (nc + 1) * 32U * 4 <= 6.5 KB
             const int U = (nc + 1) * 32 * 8 * 4 <= kTileB ? 8 : (nc + 1) * 32 * 4 * 4 <= kTileB ? 4
                         : (nc + 1) * 32 * 2 * 4 <= kTileB ? 2 : 1;
             const CUtensorMap tm = make_map(V, ld, nc, 32 * U);
