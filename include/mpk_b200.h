@@ -306,6 +306,18 @@ int mpk_precond_apply(const mpk_precond *M, const void *v, void *out, void *stre
 int mpk_block_lu(const mpk_matrix *A, int32_t k, void *lu, int32_t *piv, void *minpiv, double *thr, int32_t *bad,
                  void *stream);
 
+/*
+ * Stencil assembly on the device (replaces generate_stencil's numpy
+ * assembly, pkg/src/mpkrylov/stencils.py:192-207): the binary64 CSR arrays
+ * of the STENCIL operator S (whole matrix, row0 = 0), bit-identical to the
+ * reference's (column order = displacement order, Dirichlet truncation).
+ * row_ptr: n + 1 int64; col_idx: nnz int32; values: nnz doubles; work:
+ * mpk_stencil_assemble_ws_bytes(n) bytes.
+ */
+int mpk_stencil_assemble(const mpk_matrix *S, int64_t *row_ptr, int32_t *col_idx, double *values, void *work,
+                         void *stream);
+int64_t mpk_stencil_assemble_ws_bytes(int64_t n);
+
 /* ------------------------------------------------------------------ */
 /* host-side setup                                                     */
 /* ------------------------------------------------------------------ */

@@ -31,7 +31,7 @@ EXPORTS = (
     "mpk_lsq_solve", "mpk_vdiv", "mpk_launch_count", "mpk_fused_prof_read", "mpk_comm_part_bytes",
     "mpk_dev_alloc", "mpk_dev_free", "mpk_ipc_get", "mpk_ipc_open", "mpk_ipc_close", "mpk_rcm_host",
     "mpk_last_cycle_kernel", "mpk_can_access_peer", "mpk_comm_push_rows", "mpk_comm_reduce_ctl",
-    "mpk_block_lu",
+    "mpk_block_lu", "mpk_stencil_assemble", "mpk_stencil_assemble_ws_bytes",
 )
 MAX_RANKS = 8
 
@@ -140,6 +140,8 @@ _SIGS["mpk_lsq_init"] = (_I32, [_I32, _I32, ctypes.c_double, ctypes.c_double, _P
 _SIGS["mpk_lsq_update"] = (_I32, [_I32, _I32, _I32, _P, _P, _P, _P, _P, _P])
 _SIGS["mpk_lsq_solve"] = (_I32, [_I32, _I32, _I32, _P, _P, _P])
 _SIGS["mpk_block_lu"] = (_I32, [ctypes.POINTER(MpkMatrix), _I32, _P, _P, _P, _P, _P, _P])
+_SIGS["mpk_stencil_assemble"] = (_I32, [ctypes.POINTER(MpkMatrix), _P, _P, _P, _P, _P])
+_SIGS["mpk_stencil_assemble_ws_bytes"] = (_I64, [_I64])
 
 
 def load(require_device: bool = True):

@@ -1249,6 +1249,31 @@ int mpk_block_lu(const mpk_matrix *A, int32_t k, void *lu, int32_t *piv, void *m
     return A->dtype == MPK_F64 ? go(double{}) : go(float{});
 }
 
+int mpk_stencil_assemble(const mpk_matrix *S, int64_t *row_ptr, int32_t *col_idx, double *values, void *work,
+                         void *stream) {
+    if (!S || S->kind != MPK_STENCIL || !row_ptr || !col_idx || !values || !work)
+        return fail(MPK_EARG, "null argument or not a stencil");
+    if (S->row0 != 0) return fail(MPK_EARG, "assembly of a whole matrix only (row0 = 0)");
+    cudaStream_t s = (cudaStream_t)stream;
+    const StencilOp<double> op = make_stencil<double>(S);
+    const int64_t n = op.n;
+    if (n == 0) return MPK_OK;
+    int32_t *cnt = (int32_t *)work;
+    int64_t *bsum = (int64_t *)((char *)work + ((n * 4 + 255) / 256) * 256);
+    const int64_t nb = (n + kScanChunk - 1) / kScanChunk;
+    int g = grid_for(k_stencil_count<double>, 0, n);
+    k_stencil_count<double><<<g, kBlock, 0, s>>>(op, cnt);
+    k_scan_local<<<(unsigned)nb, kScanThreads, 0, s>>>(cnt, n, row_ptr, bsum);
+    k_scan_blocks<<<1, kScanThreads, 0, s>>>(bsum, nb);
+    k_scan_add<<<g, kBlock, 0, s>>>(row_ptr, n, bsum);
+    k_stencil_fill<double><<<g, kBlock, 0, s>>>(op, row_ptr, col_idx, values);
+    return check_launch("k_stencil_fill");
+}
+
+int64_t mpk_stencil_assemble_ws_bytes(int64_t n) {
+    return ((n * 4 + 255) / 256) * 256 + ((n + kScanChunk - 1) / kScanChunk) * 8 + 256;
+}
+
 int64_t mpk_launch_count(void) { return (int64_t)g_launches; }
 const char *mpk_last_cycle_kernel(void) { return g_last_cycle; }
 

@@ -778,6 +778,105 @@ __global__ void __launch_bounds__(kLuWarps * 32) k_block_lu(CsrOp<T> A, int k, d
     }
 }
 
+// ---------------------------------------------------------------------------
+// Stencil assembly on the device (generate_stencil, stencils.py:192-207):
+// per-row entry counts, an exclusive scan to row_ptr (int64), then each row's
+// (column, value) pairs in the reference's order -- bit-identical arrays.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(kBlock) k_stencil_count(StencilOp<T> A, int32_t *__restrict__ cnt) {
+    for (int64_t r = gtid(); r < A.n; r += gstride()) cnt[r] = A.row_entries(r, [](int64_t, T) {});
+}
+
+constexpr int kScanThreads = 1024, kScanPer = 8, kScanChunk = kScanThreads * kScanPer;
+// rp[i + 1] = cnt[0] + ... + cnt[i] within each kScanChunk block; bsum[b] = block total
+__global__ void __launch_bounds__(kScanThreads) k_scan_local(const int32_t *__restrict__ cnt, int64_t n,
+                                                             int64_t *__restrict__ rp, int64_t *__restrict__ bsum) {
+    __shared__ int64_t sw[kScanThreads / 32];
+    const int64_t base = (int64_t)blockIdx.x * kScanChunk + (int64_t)threadIdx.x * kScanPer;
+    int64_t v[kScanPer];
+    int64_t run = 0;
+#pragma unroll
+    for (int e = 0; e < kScanPer; ++e) {
+        run += (base + e < n) ? cnt[base + e] : 0;
+        v[e] = run;
+    }
+    // exclusive scan of the per-thread totals over the block
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t x = run;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) sw[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        int64_t w = sw[lane];
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        sw[lane] = w;
+    }
+    __syncthreads();
+    const int64_t off = (x - run) + (warp ? sw[warp - 1] : 0);
+#pragma unroll
+    for (int e = 0; e < kScanPer; ++e)
+        if (base + e < n) rp[base + e + 1] = v[e] + off;
+    if (threadIdx.x == kScanThreads - 1) bsum[blockIdx.x] = off + run;
+}
+
+// one block: exclusive prefix of the block totals (sequential per thread
+// over a strided slice, then a block scan), then the offsets are added
+__global__ void __launch_bounds__(kScanThreads) k_scan_blocks(int64_t *bsum, int64_t nb) {
+    __shared__ int64_t sw[kScanThreads / 32];
+    const int64_t per = (nb + kScanThreads - 1) / kScanThreads;
+    const int64_t b0 = (int64_t)threadIdx.x * per;
+    int64_t run = 0;
+    for (int64_t b = b0; b < b0 + per && b < nb; ++b) run += bsum[b];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t x = run;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) sw[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        int64_t w = sw[lane];
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        sw[lane] = w;
+    }
+    __syncthreads();
+    int64_t acc = (x - run) + (warp ? sw[warp - 1] : 0);
+    for (int64_t b = b0; b < b0 + per && b < nb; ++b) {
+        const int64_t t = bsum[b];
+        bsum[b] = acc;   // exclusive offset of block b
+        acc += t;
+    }
+}
+
+__global__ void k_scan_add(int64_t *__restrict__ rp, int64_t n, const int64_t *__restrict__ boff) {
+    for (int64_t i = gtid(); i < n; i += gstride()) rp[i + 1] += boff[i / kScanChunk];
+    if (gtid() == 0) rp[0] = 0;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kBlock) k_stencil_fill(StencilOp<T> A, const int64_t *__restrict__ rp,
+                                                         int32_t *__restrict__ ci, T *__restrict__ val) {
+    for (int64_t r = gtid(); r < A.n; r += gstride()) {
+        int64_t p = rp[r];
+        A.row_entries(r, [&](int64_t c, T v) {
+            ci[p] = (int32_t)c;
+            val[p] = v;
+            ++p;
+        });
+    }
+}
+
 // GMRES polynomial, real root: acc += inv*work ; work_next = work - inv*(A work)
 template <typename T, class Op>
 __global__ void __launch_bounds__(kBlock) k_poly_real(Op A, const T *__restrict__ work, T *__restrict__ wnext,

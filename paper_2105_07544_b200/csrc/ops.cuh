@@ -321,6 +321,67 @@ template <typename T> struct StencilOp {
         group_load(r, xv, xs, in);
         group_eval(r, in, out);
     }
+    // Stored entries of row r in the reference's column order
+    // (generate_stencil, stencils.py:192-207: displacement order, Dirichlet
+    // truncation): emit(col, value) with the coefficients row() multiplies
+    // by (double for the binary64 assembly).  Returns the entry count.
+    template <class F> __device__ __forceinline__ int row_entries(int64_t r, F &&emit) const {
+        const uint32_t g = (uint32_t)(k.row0 + r);
+        const int nx = k.nx;
+        const uint32_t q1 = k.dnx.div(g);
+        const int ix = (int)(g - q1 * (uint32_t)nx);
+        int cnt = 0;
+        auto put = [&](bool ok, int64_t c, T v) {
+            if (ok) {
+                emit(c, v);
+                ++cnt;
+            }
+        };
+        if (k.preset == MPK_LAPLACE3D) {
+            const int64_t nxy = (int64_t)nx * nx;
+            const uint32_t iz_ = k.dnxy.div(g);
+            const int iy = (int)(q1 - iz_ * (uint32_t)nx), iz = (int)iz_;
+            put(iz > 0, r - nxy, cT[0]);
+            put(iy > 0, r - nx, cT[1]);
+            put(ix > 0, r - 1, cT[2]);
+            put(true, r, cT[3]);
+            put(ix < nx - 1, r + 1, cT[4]);
+            put(iy < nx - 1, r + nx, cT[5]);
+            put(iz < nx - 1, r + nxy, cT[6]);
+            return cnt;
+        }
+        const int iy = (int)q1;
+        if (k.preset == MPK_STRETCHED2D) {
+            const bool W = ix > 0, E = ix < nx - 1, S = iy > 0, N = iy < nx - 1;
+            put(W && S, r - nx - 1, cT[0]);
+            put(S, r - nx, cT[1]);
+            put(E && S, r - nx + 1, cT[2]);
+            put(W, r - 1, cT[3]);
+            put(true, r, cT[4]);
+            put(E, r + 1, cT[5]);
+            put(W && N, r + nx - 1, cT[6]);
+            put(N, r + nx, cT[7]);
+            put(E && N, r + nx + 1, cT[8]);
+            return cnt;
+        }
+        T c0 = cT[0], c1 = cT[1], c2 = cT[2], c3 = cT[3], c4 = cT[4];
+        if (k.preset == MPK_BENTPIPE2D) {
+            const double px = __dmul_rn((double)(ix + 1), k.h);
+            const double py = __dmul_rn((double)(iy + 1), k.h);
+            const double ux = __dmul_rn(__dmul_rn(k.cc2, py), __dsub_rn(1.0, __dmul_rn(px, px)));
+            const double uy = __dmul_rn(__dmul_rn(k.ncc2, px), __dsub_rn(1.0, __dmul_rn(py, py)));
+            c0 = RN<T>::from_double(__dsub_rn(-1.0, __dmul_rn(k.hh, uy)));
+            c1 = RN<T>::from_double(__dsub_rn(-1.0, __dmul_rn(k.hh, ux)));
+            c3 = RN<T>::from_double(__dadd_rn(-1.0, __dmul_rn(k.hh, ux)));
+            c4 = RN<T>::from_double(__dadd_rn(-1.0, __dmul_rn(k.hh, uy)));
+        }
+        put(iy > 0, r - nx, c0);
+        put(ix > 0, r - 1, c1);
+        put(true, r, c2);
+        put(ix < nx - 1, r + 1, c3);
+        put(iy < nx - 1, r + nx, c4);
+        return cnt;
+    }
     // lane-per-row over [r0, r0 + 32) (interface of CsrOp::warp_rows)
     template <class X> __device__ __forceinline__ T warp_rows(int64_t r0, int64_t rend, X x, T *) const {
         const int64_t r = r0 + (threadIdx.x & 31);

@@ -109,8 +109,15 @@ def stencil_dimensions(spec: ProblemSpec):
     return spec.n, int(mask.sum())
 
 
-def generate_stencil(spec: ProblemSpec) -> CsrMatrix:
-    """Assemble the preset in binary64 (reference stencils.py:192-207)."""
+def generate_stencil(spec: ProblemSpec, on_device: bool = False) -> CsrMatrix:
+    """Assemble the preset in binary64 (reference stencils.py:192-207).
+
+    on_device=True assembles on the GPU (``mpk_stencil_assemble``: entry
+    counts, a scan, then every row's entries with the operator's own
+    coefficient arithmetic) and keeps the device copy; the host arrays are
+    the same bits as the numpy assembly (tests/test_gpu_assembly.py)."""
+    if on_device:
+        return _generate_on_device(spec)
     node, ix, disp, mask = _layout(spec)
     vals = _values(spec, node, ix)
     keep = mask.ravel()
@@ -121,4 +128,38 @@ def generate_stencil(spec: ProblemSpec) -> CsrMatrix:
     A = CsrMatrix(spec.n, row_ptr, col_idx, values, validate=False)
     A.stencil = StencilInfo(spec.preset, spec.nx, spec.diffusion, spec.velocity,
                             spec.convection_strength, spec.stretch_factor)
+    return A
+
+
+_WIDTH = {"Laplace2D": 5, "Laplace3D": 7, "UniFlow2D": 5, "BentPipe2D": 5, "Stretched2D": 9}
+
+
+def _generate_on_device(spec: ProblemSpec) -> CsrMatrix:
+    import ctypes
+
+    from . import _lib
+    from . import device as D
+    from .sparse import _DeviceCsr
+
+    t = D.torch()
+    n = spec.n
+    info = StencilInfo(spec.preset, spec.nx, spec.diffusion, spec.velocity, spec.convection_strength,
+                       spec.stretch_factor)
+    d = _lib.MpkMatrix()
+    d.kind, d.dtype, d.n, d.row0 = _lib.STENCIL, _lib.F64, n, 0
+    d.preset, d.nx = _lib.PRESET_IDS[spec.preset], spec.nx
+    d.diffusion, d.velocity, d.convection, d.stretch = info.diffusion, info.velocity, info.convection, info.stretch
+    cap = _WIDTH[spec.preset] * n
+    rp = D.empty(n + 1, t.int64)
+    ci = D.empty(cap, t.int32)
+    va = D.empty(cap, t.float64)
+    lib = D.lib()
+    ws = D.empty(int(lib.mpk_stencil_assemble_ws_bytes(n)), t.uint8)
+    _lib.check(lib.mpk_stencil_assemble(ctypes.byref(d), D.ptr(rp), D.ptr(ci), D.ptr(va), D.ptr(ws), D.stream()))
+    row_ptr = D.to_host(rp)
+    nnz = int(row_ptr[-1])
+    ci, va = ci[:nnz], va[:nnz]
+    A = CsrMatrix(n, row_ptr, D.to_host(ci).astype(np.int64), D.to_host(va), validate=False)
+    A.stencil = info
+    A._dev = _DeviceCsr(rp.to(t.int32), ci, va)
     return A
