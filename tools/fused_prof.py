@@ -16,7 +16,8 @@ P = mk.Precision
 prec = P.binary32 if a.prec == "fp32" else P.binary64
 Al = mk.convert_matrix(A, prec)
 b = torch.ones(A.n, dtype=prec.torch_dtype, device="cuda")
-cfg = mk.SolverConfig(m=50, rtol=1e-30 if prec is P.binary64 else 1e-7, precision=prec)
+cfg = mk.SolverConfig(m=50, rtol=1e-30 if prec is P.binary64 else 1e-7, precision=prec,
+                      breakdown_rule="u" if a.config == "C4" else "n_u")
 mk.gmres_cycle(Al, None, b, torch.zeros_like(b), cfg)
 ws = CycleWorkspace.get(A.n, 50, prec)
 ws.flags = 8

@@ -61,4 +61,12 @@ def dist(orth, solver):
 if "--dist" in sys.argv:
     for orth in ("cgs2", "dcgs2"):
         print("dist", orth, dist(orth, "fp64"), dist(orth, "ir"))
+inner_b = mk.SolverConfig(m=50, rtol=1e-4, precision=P.binary32, max_iters=100, basis_precision="bfloat16")
+print("bfloat16 basis ir", mk.gmres_ir(A, b, np.zeros(A.n), mk.IrConfig(inner=inner_b, rtol=1e-10)).total_iters)
+Ad = mk.generate_stencil(mk.ProblemSpec("Laplace3D", 12), on_device=True)
+Ad.use_stencil = False
+print("assembly + short-row CSR spmv", float(mk.spmv(Ad, np.ones(Ad.n)).sum()))
+Mp = mk.build_gmres_poly(mk.convert_matrix(A, P.binary32), 8, np.ones(A.n, np.float32))
+inner_p = mk.SolverConfig(m=30, rtol=1e-4, precision=P.binary32, max_iters=60)
+print("fused poly ir", mk.gmres_ir(A, b, np.zeros(A.n), mk.IrConfig(inner=inner_p, rtol=1e-10), M=Mp).total_iters)
 print("sanitize ok")
