@@ -36,14 +36,14 @@ template <typename T> struct XCg {
 
 // kDcDots2:   a0[i] += V[:, c].u, a1[i] += V[:, c].z, e0 += u.u, e1 += u.z
 // kDcUpdate2: q = (u - V X0)/rho -> qout ; u' = (z - V Y - u tau)/rho -> u (in place)
-template <typename T, int MODE, int U>
+template <typename T, int MODE, int U, int KU>
 __device__ __forceinline__ void dc_phase_u(const T *V, int64_t ld, int nc, int64_t rb, int64_t re, T *u, const T *z,
                                            T *qout, const T *X0, const T *Y, T rho, T tau,
                                            T (&a0)[RegCfg<T>::KP], T (&a1)[RegCfg<T>::KP], T &e0, T &e1, bool rev,
                                            const CommArgs<T> *cm) {
     using C = RegCfg<T>;
     constexpr int R = C::R;
-    constexpr int KU = C::KP / U;
+    static_assert(KU <= C::KP, "columns per part");
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane % C::G, p = lane / C::G;
     constexpr int64_t TRIP = (int64_t)C::WR * U;
@@ -147,9 +147,16 @@ __device__ __forceinline__ void dc_phase(const T *V, int64_t ld, int nc, int64_t
                                          T (&a1)[RegCfg<T>::KP], T &e0, T &e1, bool rev, const CommArgs<T> *cm) {
     using C = RegCfg<T>;
     const int ncp = (nc + C::P - 1) / C::P;
-    if (ncp * 4 <= C::KP) dc_phase_u<T, MODE, 4>(V, ld, nc, rb, re, u, z, qout, X0, Y, rho, tau, a0, a1, e0, e1, rev, cm);
-    else if (ncp * 2 <= C::KP) dc_phase_u<T, MODE, 2>(V, ld, nc, rb, re, u, z, qout, X0, Y, rho, tau, a0, a1, e0, e1, rev, cm);
-    else dc_phase_u<T, MODE, 1>(V, ld, nc, rb, re, u, z, qout, X0, Y, rho, tau, a0, a1, e0, e1, rev, cm);
+#define MPK_DC_U(UU, KK) dc_phase_u<T, MODE, UU, KK>(V, ld, nc, rb, re, u, z, qout, X0, Y, rho, tau, a0, a1, e0, e1, rev, cm)
+    switch (ncp) {
+        case 1: case 2: case 3: MPK_DC_U(4, 3); break;
+        case 4: MPK_DC_U(3, 4); break;
+        case 5: case 6: MPK_DC_U(2, 6); break;
+        case 7: MPK_DC_U(2, 7); break;
+        case 8: MPK_DC_U(2, 8); break;
+        default: MPK_DC_U(1, 13); break;
+    }
+#undef MPK_DC_U
 }
 
 // ... scaled by a diagonal right preconditioner: x = M u = u / a_ii

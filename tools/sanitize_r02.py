@@ -66,7 +66,9 @@ print("bfloat16 basis ir", mk.gmres_ir(A, b, np.zeros(A.n), mk.IrConfig(inner=in
 Ad = mk.generate_stencil(mk.ProblemSpec("Laplace3D", 12), on_device=True)
 Ad.use_stencil = False
 print("assembly + short-row CSR spmv", float(mk.spmv(Ad, np.ones(Ad.n)).sum()))
-Mp = mk.build_gmres_poly(mk.convert_matrix(A, P.binary32), 8, np.ones(A.n, np.float32))
+L2 = mk.generate_stencil(mk.ProblemSpec("Laplace2D", 40))
+Mp = mk.build_gmres_poly(mk.convert_matrix(L2, P.binary32), 6, np.ones(L2.n, np.float32))
 inner_p = mk.SolverConfig(m=30, rtol=1e-4, precision=P.binary32, max_iters=60)
-print("fused poly ir", mk.gmres_ir(A, b, np.zeros(A.n), mk.IrConfig(inner=inner_p, rtol=1e-10), M=Mp).total_iters)
+print("fused poly ir", mk.gmres_ir(L2, np.ones(L2.n), np.zeros(L2.n), mk.IrConfig(inner=inner_p, rtol=1e-10),
+                                   M=Mp).total_iters)
 print("sanitize ok")
