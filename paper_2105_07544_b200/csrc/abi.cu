@@ -704,6 +704,19 @@ int launch_fused_reg(const Op &op, const mpk_cycle_desc *d, int cap, double tf, 
     if (d->M && d->M->kind == MPK_PC_JACOBI && d->M->block == 1 && d->M->dtype == d->dtype)
         fa.diag = (const T *)d->M->lu;
     if (int rc = fill_comm<T>(fa, d, grid)) return rc;
+    if constexpr (Op::kStencil) {
+        // 3-D stencils reach +-nx^2 rows, about a CTA's slab at C4: one more
+        // grid barrier per step lets the SpMV read v_k's halo from the stored
+        // column instead of dividing w'' by beta again (MPK_VK_SYNC=0/1 overrides)
+        static int force = -2;
+        if (force == -2) {
+            const char *e = getenv("MPK_VK_SYNC");
+            force = e ? atoi(e) : -1;
+        }
+        const int64_t reach = op.k.preset == MPK_LAPLACE3D ? (int64_t)op.k.nx * op.k.nx : (int64_t)op.k.nx + 1;
+        const int64_t rpc = ((d->n + grid - 1) / grid + 63) / 64 * 64;
+        fa.vk_sync = (!multi && !poly && (force >= 0 ? force : (2 * reach > rpc && rpc >= 16384))) ? 1 : 0;
+    }
     Op opc = op;
     void *args[] = {(void *)&opc, (void *)&fa};
     ProfScope ps(7, 0.0, s);

@@ -71,6 +71,7 @@ template <typename T> struct FusedArgs {
     const T *diag;    // k_cycle_reg: diagonal right preconditioner a_ii (block Jacobi k = 1), or nullptr
     T *z;             // k_cycle_reg: z = v_k / a_ii for the CTA's own rows
     T vs = T(1), vsi = T(1);   // k_cycle_reg, binary16 basis: stored = v * vs (power of two), vsi = 1 / vs
+    int vk_sync = 0;           // k_cycle_reg: grid barrier after v_k, all SpMV inputs from the stored column
     // k_cycle_reg with a GMRES-polynomial right preconditioner (npoly > 0):
     // z = p(A) v_k and the correction's p(A) (V_k d) evaluated in-kernel,
     // one grid barrier per SpMV; pw0/pw1 ping-pong the product-form work

@@ -628,6 +628,13 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_reg(Op A, FusedArgs<T> a) {
             poly_apply_dev<T>(A, MPK_POLY_BUFS, reinterpret_cast<const T *>(vk), rb, re, sstage);
             MPK_SYNC_OR_ABORT();   // z complete
             an = poly_spmv_dev<T>(A, a.pacc, a.w, rb, re, sstage);
+        } else if (!MULTI && a.vk_sync) {
+            // wide halo (3-D stencils: +-nx^2 rows, about a CTA's slab):
+            // make v_k (and z) complete on every CTA, then read every SpMV
+            // input from the stored column instead of re-forming the halo
+            // as w''/beta -- the same values, without a division each
+            MPK_SYNC_OR_ABORT();
+            an = phase_a_spmv<T>(A, XSlab<T, TV>{src, vk, dv, 0, a.n, a.diag, a.z, vs, vsi}, a.w, rb, re, sstage);
         } else {
             an = phase_a_spmv<T>(A, XSlab<T, TV>{src, vk, dv, rb, re, a.diag, a.z, vs, vsi}, a.w, rb, re, sstage);
         }
