@@ -496,6 +496,77 @@ def one_cycle(A, M, b, x0, m, tol, r0=None, scale=None, cap=None, rule="n_u", ba
     return x, CycleOut(k, rels, sc, brk)
 
 
+def dcgs2_cycle(A, M, b, x0, m, tol, r0=None, scale=None, cap=None, rule="n_u", basis16=False):
+    """gmres_cycle with this repo's lagged one-reduction CGS2
+    (SolverConfig.orthogonalization = "dcgs2"; not a reference feature: the
+    reference's CGS2 of kernels.py:98-126 reordered so each step needs one
+    reduction, fused_dcgs2.cuh).  Step j, with Q_j final and the candidate
+    u = w_{j-1} - Q_j c after its first pass:
+      z = A u ; X0 = Q_j^T u ; X1 = Q_j^T z ; a = u.u ; b = u.z
+      rho = sqrt(a - X0.X0)      (clamped at 1e-3 a / 1e-11 a: cycle ends)
+      H[:, j-1] = [c + X0; rho]  (the append test on ||w_{j-1}||^2 = a + c.c)
+      t = (b - X0.X1)/rho, tau = t/rho, c' = ([X1; t] - H X0)/rho
+      q_j = (u - Q_j X0)/rho ; u' = (z - Q_j (X1 - X0 tau) - u tau)/rho
+    basis16 as in one_cycle (q_j stored rounded); M must be None."""
+    assert M is None, "dcgs2 restatement: identity preconditioner"
+    rp, ci, vals = A
+    dt = vals.dtype
+    sp = lambda x: spmv_seq(rp, ci, vals, x)
+    r = b - sp(x0) if r0 is None else r0
+    gam = nrm(r)
+    sc = float(gam) if scale is None else float(scale)
+    steps_cap = m if cap is None else max(1, min(m, int(cap)))
+    if float(gam) == 0.0:
+        return x0.copy(), CycleOut(0, [], sc if sc > 0 else 1.0, False)
+    n = b.shape[0]
+    u_rnd = unit_roundoff(dt)
+    s16 = basis16_scale(n)
+    rnd = (lambda v: round_bf16(v, s16)) if basis16 == "bfloat16" else (lambda v: round16(v, s16))
+    store = rnd if basis16 else (lambda v: v)
+    eta = dt.type(1e-3 if dt == np.float32 else 1e-11)
+    Q = np.zeros((n, steps_cap + 1), dtype=dt, order="F")
+    H = np.zeros((steps_cap + 1, steps_cap), dtype=dt)
+    Q[:, 0] = store(r / gam)
+    w = sp(Q[:, 0])
+    c = Q[:, :1].T @ w
+    u = w - Q[:, :1] @ c
+    lsq = RotatedLsq(steps_cap, gam, sc, dt)
+    rels = []
+    brk = False
+    k = 0
+    for j in range(1, steps_cap + 1):
+        z = sp(u)
+        X0 = Q[:, :j].T @ u
+        X1 = Q[:, :j].T @ z
+        a, bb = np.dot(u, u), np.dot(u, z)
+        rho2 = a - np.dot(X0, X0)
+        trunc = not rho2 > eta * a
+        if trunc:
+            rho2 = eta * a
+        rho = np.sqrt(rho2)
+        H[:j, j - 1] = c + X0
+        H[j, j - 1] = rho
+        limit = (n * u_rnd if rule == "n_u" else u_rnd) * float(np.sqrt(a + np.dot(c, c)))
+        ok = float(rho) > limit
+        rel = lsq.push(H[:j, j - 1], rho)
+        rels.append(rel)
+        k = j
+        if not ok:
+            brk = True
+            break
+        if rel <= tol or trunc or j == steps_cap:
+            break
+        t = (bb - np.dot(X0, X1)) / rho
+        tau = t / rho
+        c = (np.append(X1, t) - H[:j + 1, :j] @ X0) / rho
+        Q[:, j] = store((u - Q[:, :j] @ X0) / rho)
+        u = (z - Q[:, :j] @ (X1 - X0 * tau) - u * tau) / rho
+    d, err = lsq.back_solve(k)
+    if err is not None:
+        raise ArithmeticError("triangular breakdown", *err)
+    return x0 + Q[:, :k] @ d, CycleOut(k, rels, sc, brk)
+
+
 def restarted(A, M, b, x0, m=50, rtol=1e-10, max_iters=100_000, max_restarts=1_000_000,
               baseline=None, restart_on_loss=True, phase=None, rule="n_u"):
     """gmres_restarted (gmres.py:221-308)."""
@@ -540,8 +611,10 @@ def restarted(A, M, b, x0, m=50, rtol=1e-10, max_iters=100_000, max_restarts=1_0
 
 
 def refine(A64, b, x0, m=50, rtol=1e-10, inner_max_iters=100_000, max_refinements=1_000_000,
-           M=None, A32=None, rule="n_u", basis16=False):
-    """gmres_ir (multiprecision.py:120-233): fp64 outer, fp32 inner cycles."""
+           M=None, A32=None, rule="n_u", basis16=False, orth="cgs2"):
+    """gmres_ir (multiprecision.py:120-233): fp64 outer, fp32 inner cycles
+    (orth="dcgs2": inner cycles with dcgs2_cycle)."""
+    cycle = dcgs2_cycle if orth == "dcgs2" else one_cycle
     rp, ci, v64 = A64
     if A32 is None:
         A32 = (rp, ci, v64.astype(np.float32))
@@ -576,7 +649,7 @@ def refine(A64, b, x0, m=50, rtol=1e-10, inner_max_iters=100_000, max_refinement
                 stalled = True
                 break
             continue
-        u32, st = one_cycle(A32, M, r32, z32, m, floor, r0=r32, cap=left, rule=rule, basis16=basis16)
+        u32, st = cycle(A32, M, r32, z32, m, floor, r0=r32, cap=left, rule=rule, basis16=basis16)
         hist.extend((total + i + 1, "inner", rel * r32n / base, None)
                     for i, rel in enumerate(st.implicit))
         total += st.steps

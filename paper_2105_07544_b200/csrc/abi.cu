@@ -732,12 +732,17 @@ int launch_fused_reg(const Op &op, const mpk_cycle_desc *d, int cap, double tf, 
 
 // Lagged one-reduction CGS2 (desc flag bit 4, SolverConfig.orthogonalization
 // = "dcgs2"): identity preconditioner, m <= 51, one GPU.
-template <typename T, class Op>
+// TV: basis storage (T, or a 16-bit basis on one GPU, flags 32 / 64).
+template <typename T, class Op, typename TV = T>
 int launch_dcgs2(const Op &op, const mpk_cycle_desc *d, int cap, double tf, double u, cudaStream_t s) {
     const int m = d->m;
     T *w = (T *)d->work;
     Ws ws = carve(d->ws);
-    auto kern = d->nranks > 1 ? k_cycle_dcgs2<T, Op, true> : k_cycle_dcgs2<T, Op, false>;
+    constexpr bool half = sizeof(TV) != sizeof(T);
+    auto kern = k_cycle_dcgs2<T, Op, false, TV>;
+    if constexpr (!half) {
+        if (d->nranks > 1) kern = k_cycle_dcgs2<T, Op, true, TV>;
+    }
     const size_t smem = sizeof(T) * (2 * (size_t)(m + 1) * m + 2 * m + (m + 1) + 5 * 64 + kFW * kFSlots +
                                      kFW * kCsrWarpBuf);
     static size_t attr_set[2] = {0, 0};
@@ -780,6 +785,13 @@ int launch_dcgs2(const Op &op, const mpk_cycle_desc *d, int cap, double tf, doub
     fa.u = u;
     fa.diag = nullptr;
     fa.z = w + 3 * d->ld;
+    fa.vs = fa.vsi = T(1);
+    if constexpr (half) {
+        // the same power-of-two scale as k_cycle_reg's 16-bit basis
+        const double e = std::nearbyint(0.5 * std::log2((double)(d->n > 1 ? d->n : 1)));
+        fa.vs = (T)std::ldexp(1.0, (int)e);
+        fa.vsi = (T)std::ldexp(1.0, -(int)e);
+    }
     if (d->M && d->M->kind == MPK_PC_JACOBI && d->M->block == 1 && d->M->dtype == d->dtype)
         fa.diag = (const T *)d->M->lu;
     if (int rc = fill_comm<T>(fa, d, grid)) return rc;
@@ -791,7 +803,8 @@ int launch_dcgs2(const Op &op, const mpk_cycle_desc *d, int cap, double tf, doub
         g_err = std::string("k_cycle_dcgs2: ") + cudaGetErrorString(e);
         return MPK_ELAUNCH;
     }
-    g_last_cycle = d->nranks > 1 ? "k_cycle_dcgs2/multi" : "k_cycle_dcgs2";
+    g_last_cycle = half ? (std::is_same<TV, __half>::value ? "k_cycle_dcgs2/half" : "k_cycle_dcgs2/bf16")
+                        : d->nranks > 1 ? "k_cycle_dcgs2/multi" : "k_cycle_dcgs2";
     return check_launch("k_cycle_dcgs2");
 }
 
@@ -836,12 +849,17 @@ template <typename T> int run_cycle(const mpk_cycle_desc *d, cudaStream_t s) {
         // 16-bit basis storage (SolverConfig.basis_precision = "binary16" /
         // "bfloat16")
         if constexpr (sizeof(T) == 4) {
-            const bool ok = (!precond || diag1) && !(d->flags & 16) && !(d->flags & 4) && d->nranks <= 1 &&
+            const bool ok = (!precond || diag1) && !(d->flags & 4) && d->nranks <= 1 &&
                             m + 1 <= kRegMaxCols && (uintptr_t)d->x_out % 16 == 0 && (uintptr_t)d->V % 16 == 0 &&
                             (uintptr_t)d->work % 16 == 0 && (uintptr_t)d->r0 % 16 == 0 &&
                             (d->flags & (32 | 64)) != (32 | 64);
             if (!ok)
-                return fail(MPK_EUNSUPPORTED, "16-bit basis: one GPU, m <= 51, CGS2, identity or Jacobi(1)");
+                return fail(MPK_EUNSUPPORTED, "16-bit basis: one GPU, m <= 51, identity or Jacobi(1)");
+            if (d->flags & 16)   // lagged one-reduction CGS2 over the 16-bit basis
+                return with_op<T>(d->A, [&](auto op) -> int {
+                    if (d->flags & 64) return launch_dcgs2<T, decltype(op), __nv_bfloat16>(op, d, cap, tf, u, s);
+                    return launch_dcgs2<T, decltype(op), __half>(op, d, cap, tf, u, s);
+                });
             return with_op<T>(d->A, [&](auto op) -> int {
                 if (d->flags & 64) return launch_fused_reg<T, decltype(op), __nv_bfloat16>(op, d, cap, tf, u, s);
                 return launch_fused_reg<T, decltype(op), __half>(op, d, cap, tf, u, s);
@@ -1064,6 +1082,39 @@ int mpk_spmv(const mpk_matrix *A, const void *x, void *y, void *stream) {
                     int g = grid_for(kw, smem, (op.n + kSpmvChunk - 1) / kSpmvChunk * kBlock);
                     kw<<<g, kBlock, smem, s>>>(op, (const T *)x, (T *)y);
                     return check_launch("k_spmv_win");
+                }
+            }
+            if constexpr (Op::kStencil) {
+                // row groups with the preset fixed at compile time
+                // (k_spmv_pre); constant-coefficient presets keep two groups'
+                // loads in flight per thread, BentPipe (double coefficient
+                // arithmetic per row) one
+                constexpr int R = 16 / (int)sizeof(T);
+                // StencilOp::group_ok() evaluated on the host side
+                const bool groups = op.k.preset != MPK_STRETCHED2D && op.k.nx % R == 0 && op.k.row0 % R == 0;
+                // MPK_SPMV_UG=0 (generic k_spmv) / 1 / 2 groups per trip: A/B
+                static int ug_env = -2;
+                if (ug_env == -2) {
+                    const char *e = getenv("MPK_SPMV_UG");
+                    ug_env = e ? atoi(e) : -1;
+                }
+                int ug = ug_env >= 0 ? ug_env : (op.k.preset == MPK_BENTPIPE2D ? 1 : 2);
+                if (ug > 0 && groups && ((uintptr_t)x % 16) == 0 && ((uintptr_t)y % 16) == 0) {
+                    void (*kp)(StencilOp<T>, const T *, T *) = nullptr;
+#define MPK_PRE(P) kp = ug == 1 ? k_spmv_pre<T, P, 1> : k_spmv_pre<T, P, 2>
+                    switch (op.k.preset) {
+                        case MPK_LAPLACE3D: MPK_PRE(MPK_LAPLACE3D); break;
+                        case MPK_LAPLACE2D: MPK_PRE(MPK_LAPLACE2D); break;
+                        case MPK_UNIFLOW2D: MPK_PRE(MPK_UNIFLOW2D); break;
+                        case MPK_BENTPIPE2D: MPK_PRE(MPK_BENTPIPE2D); break;
+                        default: break;
+                    }
+#undef MPK_PRE
+                    if (kp) {
+                        int g = grid_for(kp, 0, (op.n / R + ug - 1) / ug);
+                        kp<<<g, kBlock, 0, s>>>(op, (const T *)x, (T *)y);
+                        return check_launch("k_spmv_pre");
+                    }
                 }
             }
             auto kern = k_spmv<T, Op>;

@@ -160,6 +160,22 @@ template <typename T, int R> __device__ __forceinline__ void strows(T *p, const 
     }
 }
 
+// R consecutive elements of T stored as TV (T, or a 16-bit basis holding
+// v * vs): one 16-byte store of 8 halves, or strows
+template <typename T, typename TV, int R> __device__ __forceinline__ void stvrows(TV *p, const T (&o)[R], T vs) {
+    if constexpr (sizeof(TV) == sizeof(T)) {
+        strows<T, R>(p, o);
+    } else {
+        static_assert(R * sizeof(TV) == 16, "one 16-byte group of the 16-bit basis");
+        Pack<TV> h;
+#pragma unroll
+        for (int e = 0; e < R; ++e) h.v[e] = VIO<T, TV>::put(o[e], vs);
+        uint4 w;
+        memcpy(&w, &h, 16);
+        __stcg(reinterpret_cast<uint4 *>(p), w);
+    }
+}
+
 // Warp-level sum (fixed butterfly order -> deterministic).
 template <typename T> __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

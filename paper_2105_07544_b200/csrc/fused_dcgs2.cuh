@@ -36,13 +36,16 @@ template <typename T> struct XCg {
 
 // kDcDots2:   a0[i] += V[:, c].u, a1[i] += V[:, c].z, e0 += u.u, e1 += u.z
 // kDcUpdate2: q = (u - V X0)/rho -> qout ; u' = (z - V Y - u tau)/rho -> u (in place)
-template <typename T, int MODE, int U, int KU>
-__device__ __forceinline__ void dc_phase_u(const T *V, int64_t ld, int nc, int64_t rb, int64_t re, T *u, const T *z,
-                                           T *qout, const T *X0, const T *Y, T rho, T tau,
+// TV: basis storage (T, or binary16 holding q * vs; the scale is folded
+// into the coefficients and the dot partials as in reg_phase_u)
+template <typename T, int MODE, int U, int KU, typename TV = T>
+__device__ __forceinline__ void dc_phase_u(const TV *V, int64_t ld, int nc, int64_t rb, int64_t re, T *u, const T *z,
+                                           TV *qout, const T *X0, const T *Y, T rho, T tau,
                                            T (&a0)[RegCfg<T>::KP], T (&a1)[RegCfg<T>::KP], T &e0, T &e1, bool rev,
-                                           const CommArgs<T> *cm) {
-    using C = RegCfg<T>;
+                                           const CommArgs<T> *cm, T vs = T(1), T vsi = T(1)) {
+    using C = RegCfg<T, TV>;
     constexpr int R = C::R;
+    constexpr bool half = sizeof(TV) != sizeof(T);
     static_assert(KU <= C::KP, "columns per part");
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane % C::G, p = lane / C::G;
@@ -51,7 +54,8 @@ __device__ __forceinline__ void dc_phase_u(const T *V, int64_t ld, int nc, int64
     const int64_t ntrip = (b0 < re) ? (re - b0 + step - 1) / step : 0;
     for (int64_t t = 0; t < ntrip; ++t) {
         const int64_t b = b0 + (rev ? ntrip - 1 - t : t) * step;
-        Pack<T> vv[U][KU], uv[U], zv[U];
+        Pack<TV> vv[U][KU];
+        T uv[U][R], zv[U][R];
 #pragma unroll
         for (int uu = 0; uu < U; ++uu) {
             const int64_t r = b + (int64_t)(uu * C::G + g) * R;
@@ -62,17 +66,17 @@ __device__ __forceinline__ void dc_phase_u(const T *V, int64_t ld, int nc, int64
                 if (c < nc && live) vv[uu][i] = ldcg16(V + (int64_t)c * ld + r);
                 else {
 #pragma unroll
-                    for (int e = 0; e < R; ++e) vv[uu][i].v[e] = T(0);
+                    for (int e = 0; e < R; ++e) vv[uu][i].v[e] = TV(0.0f);
                 }
             }
             // kDcUpdate2 writes u in place from part 0: only part 0 reads it there
             const bool need = live && (MODE == kDcDots2 || p == 0);
             if (need) {
-                uv[uu] = ldcg16(u + r);
-                zv[uu] = ldcg16(z + r);
+                ldrows<T, R>(u + r, uv[uu]);
+                ldrows<T, R>(z + r, zv[uu]);
             } else {
 #pragma unroll
-                for (int e = 0; e < R; ++e) uv[uu].v[e] = zv[uu].v[e] = T(0);
+                for (int e = 0; e < R; ++e) uv[uu][e] = zv[uu][e] = T(0);
             }
         }
 #pragma unroll
@@ -83,18 +87,20 @@ __device__ __forceinline__ void dc_phase_u(const T *V, int64_t ld, int nc, int64
 #pragma unroll
                 for (int i = 0; i < KU; ++i) {
                     if (p + C::P * i < nc) {
+                        T vr[R];
+                        raw_vals<T, TV>(vv[uu][i], vr);
 #pragma unroll
                         for (int e = 0; e < R; ++e) {
-                            a0[i] += vv[uu][i].v[e] * uv[uu].v[e];
-                            a1[i] += vv[uu][i].v[e] * zv[uu].v[e];
+                            a0[i] += vr[e] * uv[uu][e];
+                            a1[i] += vr[e] * zv[uu][e];
                         }
                     }
                 }
                 if (p == 0) {
 #pragma unroll
                     for (int e = 0; e < R; ++e) {
-                        e0 += uv[uu].v[e] * uv[uu].v[e];
-                        e1 += uv[uu].v[e] * zv[uu].v[e];
+                        e0 += uv[uu][e] * uv[uu][e];
+                        e1 += uv[uu][e] * zv[uu][e];
                     }
                 }
                 continue;
@@ -106,11 +112,13 @@ __device__ __forceinline__ void dc_phase_u(const T *V, int64_t ld, int nc, int64
             for (int i = 0; i < KU; ++i) {
                 const int c = p + C::P * i;
                 if (c < nc) {
-                    const T c1 = X0[c], c2 = Y[c];
+                    const T c1 = half ? X0[c] * vsi : X0[c], c2 = half ? Y[c] * vsi : Y[c];
+                    T vr[R];
+                    raw_vals<T, TV>(vv[uu][i], vr);
 #pragma unroll
                     for (int e = 0; e < R; ++e) {
-                        s1[e] += vv[uu][i].v[e] * c1;
-                        s2[e] += vv[uu][i].v[e] * c2;
+                        s1[e] += vr[e] * c1;
+                        s2[e] += vr[e] * c2;
                     }
                 }
             }
@@ -123,31 +131,49 @@ __device__ __forceinline__ void dc_phase_u(const T *V, int64_t ld, int nc, int64
                 }
             }
             if (p == 0 && live) {
-                Pack<T> qv, un;
+                T qv[R], un[R];
 #pragma unroll
                 for (int e = 0; e < R; ++e) {
-                    qv.v[e] = RN<T>::div(RN<T>::sub(uv[uu].v[e], s1[e]), rho);
-                    un.v[e] = RN<T>::div(RN<T>::sub(RN<T>::sub(zv[uu].v[e], s2[e]), RN<T>::mul(uv[uu].v[e], tau)), rho);
+                    qv[e] = RN<T>::div(RN<T>::sub(uv[uu][e], s1[e]), rho);
+                    un[e] = RN<T>::div(RN<T>::sub(RN<T>::sub(zv[uu][e], s2[e]), RN<T>::mul(uv[uu][e], tau)), rho);
                 }
-                stcg16(qout + r, qv);
-                stcg16(u + r, un);
+                stvrows<T, TV, R>(qout + r, qv, vs);
+                strows<T, R>(u + r, un);
                 if (cm != nullptr) {   // halo rows of the candidate for the other ranks' SpMV (P2P)
                     for (int q = 0; q < cm->nranks; ++q)
                         if (q != cm->rank && r >= cm->mir_lo[q] && r < cm->mir_hi[q])
-                            stcg16(cm->xg[q] + cm->row0 + r, un);
+                            strows<T, R>(cm->xg[q] + cm->row0 + r, un);
                 }
+            }
+        }
+    }
+    if constexpr (half) {
+        if (MODE == kDcDots2) {
+#pragma unroll
+            for (int i = 0; i < KU; ++i) {
+                a0[i] *= vsi;
+                a1[i] *= vsi;
             }
         }
     }
 }
 
-template <typename T, int MODE>
-__device__ __forceinline__ void dc_phase(const T *V, int64_t ld, int nc, int64_t rb, int64_t re, T *u, const T *z,
-                                         T *qout, const T *X0, const T *Y, T rho, T tau, T (&a0)[RegCfg<T>::KP],
-                                         T (&a1)[RegCfg<T>::KP], T &e0, T &e1, bool rev, const CommArgs<T> *cm) {
+template <typename T, int MODE, typename TV = T>
+__device__ __forceinline__ void dc_phase(const TV *V, int64_t ld, int nc, int64_t rb, int64_t re, T *u, const T *z,
+                                         TV *qout, const T *X0, const T *Y, T rho, T tau, T (&a0)[RegCfg<T>::KP],
+                                         T (&a1)[RegCfg<T>::KP], T &e0, T &e1, bool rev, const CommArgs<T> *cm,
+                                         T vs = T(1), T vsi = T(1)) {
     using C = RegCfg<T>;
     const int ncp = (nc + C::P - 1) / C::P;
-#define MPK_DC_U(UU, KK) dc_phase_u<T, MODE, UU, KK>(V, ld, nc, rb, re, u, z, qout, X0, Y, rho, tau, a0, a1, e0, e1, rev, cm)
+#define MPK_DC_U(UU, KK) \
+    dc_phase_u<T, MODE, UU, KK, TV>(V, ld, nc, rb, re, u, z, qout, X0, Y, rho, tau, a0, a1, e0, e1, rev, cm, vs, vsi)
+    if constexpr (sizeof(TV) != sizeof(T)) {
+        // 8 rows per 16-byte basis group: u and z take 16 registers per
+        // group, so at most two groups per thread and trip
+        if (ncp <= 6) MPK_DC_U(2, 6);
+        else MPK_DC_U(1, 13);
+        return;
+    }
     switch (ncp) {
         case 1: case 2: case 3: MPK_DC_U(4, 3); break;
         case 4: MPK_DC_U(3, 4); break;
@@ -204,9 +230,14 @@ __device__ __forceinline__ void dc_spmv(const Op &A, const T *x, const T *diag, 
     else dc_spmv_x<T>(A, XCg<T>{x}, y, rb, re, sstage);
 }
 
-template <typename T, class Op, bool MULTI>
+template <typename T, class Op, bool MULTI, typename TV = T>
 __global__ void __launch_bounds__(kFB, 1) k_cycle_dcgs2(Op A, FusedArgs<T> a) {
+    static_assert(sizeof(TV) == sizeof(T) || !MULTI, "16-bit basis: one GPU");
     using C = RegCfg<T>;
+    using IO = VIO<T, TV>;
+    // basis storage: T, or binary16 holding q * vs (SolverConfig.basis_precision)
+    TV *const Vb = reinterpret_cast<TV *>(a.V);
+    const T vs = a.vs, vsi = a.vsi;
     extern __shared__ __align__(16) unsigned char dsm_dc[];
     const int m = a.m, ldr = m + 1;
     T *sR = reinterpret_cast<T *>(dsm_dc);     // (m+1) x m rotated columns
@@ -287,7 +318,7 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_dcgs2(Op A, FusedArgs<T> a) {
     if (!s_done) {
         // ---- prologue: q_0 = r0/gamma ; w = A q_0 ; c = q_0.w ; u = w - q_0 c
         const T gm = s_gamma;
-        T *q0 = a.V;
+        TV *q0 = Vb;
         const T *src = a.r0;
         if (multi) {
             // q_0's SpMV reads halo rows of r0: stage r0 in the x buffer, mirror
@@ -301,22 +332,23 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_dcgs2(Op A, FusedArgs<T> a) {
             MPK_DC_SYNC();
         }
         for (int64_t r = rb + tid; r < re; r += kFB) {
-            const T v = RN<T>::div(__ldcg(src + r), gm);
-            q0[r] = v;
+            const TV hv = IO::put(RN<T>::div(__ldcg(src + r), gm), vs);
+            q0[r] = hv;
+            const T v = IO::get(hv, vsi);   // as stored: the SpMV input is the stored q_0
             if (a.diag) a.z[r] = RN<T>::div(v, __ldg(a.diag + r));   // M q_0 on the own rows
         }
         __syncthreads();
-        phase_a_spmv<T>(A, XSlab<T>{src, q0, gm, rb, re, a.diag, a.z}, z, rb, re, sstage);
+        phase_a_spmv<T>(A, XSlab<T, TV>{src, q0, gm, rb, re, a.diag, a.z, vs, vsi}, z, rb, re, sstage);
         __syncthreads();
 #pragma unroll
         for (int i = 0; i < C::KP; ++i) a0[i] = T(0);
         T ext = T(0);
-        reg_phase<T, kRegDots>(a.V, a.ld, 1, rb, re, a.n, z, nullptr, nullptr, a0, ext);
+        reg_phase<T, kRegDots, TV>(Vb, a.ld, 1, rb, re, a.n, z, nullptr, nullptr, a0, ext, nullptr, nullptr, false, vsi);
         reg_write_partials<T>(a0, 1, T(0), sred, part, cmp, 0, 0, false, kXa);
         MPK_DC_SYNC();
         cross_reduce<T>(part, ncol, 1, 1, sc, pstride, kXa);   // sc[0] = c
         __syncthreads();
-        reg_phase<T, kRegUpdateNorm>(a.V, a.ld, 1, rb, re, a.n, z, u, sc, a0, ext, cmp);   // u = w - q_0 c
+        reg_phase<T, kRegUpdateNorm, TV>(Vb, a.ld, 1, rb, re, a.n, z, u, sc, a0, ext, cmp, nullptr, false, vsi);   // u = w - q_0 c
         MPK_DC_SYNC();
     }
     // ---- steps j = 1..cap: finalise column j-1, build q_j and the next candidate
@@ -326,8 +358,8 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_dcgs2(Op A, FusedArgs<T> a) {
         T e0 = T(0), e1 = T(0);
 #pragma unroll
         for (int i = 0; i < C::KP; ++i) a0[i] = a1[i] = T(0);
-        dc_phase<T, kDcDots2>(a.V, a.ld, j, rb, re, u, z, nullptr, nullptr, nullptr, T(0), T(0), a0, a1, e0, e1,
-                              j & 1, nullptr);
+        dc_phase<T, kDcDots2, TV>(Vb, a.ld, j, rb, re, u, z, nullptr, nullptr, nullptr, T(0), T(0), a0, a1, e0, e1,
+                                  j & 1, nullptr, vs, vsi);
         reg_write_partials<T>(a0, j, e0, sred, part, cmp, 0, 0, true, kXa);
         reg_write_partials<T>(a1, j, e1, sred, part, cmp, 0, kSlotB, true, kXb);
         MPK_DC_SYNC();
@@ -408,8 +440,8 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_dcgs2(Op A, FusedArgs<T> a) {
         __syncthreads();
         // ---- one update pass: q_j -> V[:, j], candidate u' in place
         T e0d = T(0), e1d = T(0);
-        dc_phase<T, kDcUpdate2>(a.V, a.ld, j, rb, re, u, z, a.V + (int64_t)j * a.ld, sX0, sY, rho, tau, a0, a1, e0d,
-                                e1d, (j + 1) & 1, cmp);
+        dc_phase<T, kDcUpdate2, TV>(Vb, a.ld, j, rb, re, u, z, Vb + (int64_t)j * a.ld, sX0, sY, rho, tau, a0, a1,
+                                    e0d, e1d, (j + 1) & 1, cmp, vs, vsi);
         MPK_DC_SYNC();
     }
 
@@ -430,7 +462,7 @@ __global__ void __launch_bounds__(kFB, 1) k_cycle_dcgs2(Op A, FusedArgs<T> a) {
         return;
     }
     T ext = T(0);
-    reg_phase<T, kRegCorrect>(a.V, a.ld, k, rb, re, a.n, a.x0, a.x_out, sd, a0, ext, nullptr, a.diag);   // x0 + M V_k d
+    reg_phase<T, kRegCorrect, TV>(Vb, a.ld, k, rb, re, a.n, a.x0, a.x_out, sd, a0, ext, nullptr, a.diag, false, vsi);   // x0 + M V_k d
 #undef MPK_DC_SYNC
 }
 

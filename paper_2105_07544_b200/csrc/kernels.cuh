@@ -524,6 +524,41 @@ __global__ void __launch_bounds__(kBlock) k_spmv(Op A, const T *__restrict__ x, 
     for_rows<T>(A, XPlain<T>{x}, sb, [&](int64_t r, T yr) { y[r] = yr; });
 }
 
+// Stencil presets in 16-byte row groups with the preset fixed at compile
+// time: PRESET is written into a local copy of the operator, so the other
+// presets' branches fold away (BentPipe's double coefficient arithmetic sets
+// k_spmv's register count for every preset), and UG groups per thread per
+// trip with every group's loads issued before any is evaluated.  Same
+// per-row sums as row() (group_eval == row()).  Needs group_ok() and 16-byte
+// aligned x / y; the host checks both.
+template <typename T, int PRESET, int UG>
+__global__ void __launch_bounds__(kBlock) k_spmv_pre(StencilOp<T> A, const T *__restrict__ x, T *__restrict__ y) {
+    constexpr int R = 16 / (int)sizeof(T);
+    StencilOp<T> B = A;
+    B.k.preset = PRESET;
+    const XPlain<T> xs{x};
+    auto xv = [&](int64_t c) { return xs.vec(c); };
+    const int64_t ng = B.n / R, st = gstride();
+    int64_t gi = gtid();
+    for (; gi + (UG - 1) * st < ng; gi += UG * st) {
+        typename StencilOp<T>::GroupIn in[UG];
+#pragma unroll
+        for (int u = 0; u < UG; ++u) B.group_load((gi + u * st) * R, xv, xs, in[u]);
+#pragma unroll
+        for (int u = 0; u < UG; ++u) {
+            Pack<T> o;
+            B.group_eval((gi + u * st) * R, in[u], o.v);
+            *reinterpret_cast<Pack<T> *>(y + (gi + u * st) * R) = o;
+        }
+    }
+    for (; gi < ng; gi += st) {
+        Pack<T> o;
+        B.row_group(gi * R, xv, xs, o.v);
+        *reinterpret_cast<Pack<T> *>(y + gi * R) = o;
+    }
+    for (int64_t r = ng * R + gtid(); r < B.n; r += st) y[r] = B.row(r, xs);
+}
+
 // Short CSR rows (<= 8 stored entries on average, e.g. the stencils in CSR
 // form): thread per row.  A warp's 32 rows cover one contiguous run of
 // entries, so each of a row's entry loads is coalesced across the warp and

@@ -68,3 +68,21 @@ def test_binary16_basis_with_jacobi1(cuda):
     base = ir(A, "working", rule="u", M=M)
     assert rep.converged and rep.final_explicit_relres <= 1e-10
     assert rep.total_iters <= 1.5 * base.total_iters + 50
+
+
+@pytest.mark.parametrize("basis", ["binary16", "bfloat16"])
+@pytest.mark.parametrize("preset,nx", [("Laplace3D", 20), ("Laplace3D", 40), ("BentPipe2D", 64)])
+def test_lagged_cgs2_over_16bit_basis_vs_oracle(cuda, preset, nx, basis):
+    """orthogonalization="dcgs2" with a 16-bit basis (k_cycle_dcgs2 over
+    binary16 / bfloat16 storage) against the oracle's dcgs2_cycle with the
+    same stored-basis rounding."""
+    A = mk.generate_stencil(mk.ProblemSpec(preset, nx))
+    inner = mk.SolverConfig(m=50, rtol=1e-4, precision=P.binary32, max_iters=20000, orthogonalization="dcgs2",
+                            basis_precision=basis)
+    rep = mk.gmres_ir(A, np.ones(A.n), np.zeros(A.n), mk.IrConfig(inner=inner, rtol=1e-10))
+    assert _lib.last_cycle_kernel() == ("k_cycle_dcgs2/half" if basis == "binary16" else "k_cycle_dcgs2/bf16")
+    rp, ci, v = O.stencil_csr(preset, nx)
+    ref = O.refine((rp, ci, v), np.ones(A.n), np.zeros(A.n), 50, 1e-10, 20000, orth="dcgs2",
+                   basis16=True if basis == "binary16" else "bfloat16")
+    assert rep.converged and ref.converged and rep.final_explicit_relres <= 1e-10
+    assert abs(rep.total_iters - ref.iters) <= 50, (rep.total_iters, ref.iters)

@@ -113,3 +113,21 @@ def test_oracle_breakdown_rule_u_matches_reference_patch(runs):
     l3 = O.stencil_csr("Laplace3D", 40)
     out = O.refine(l3, np.ones(64000), np.zeros(64000), 50, 1e-10, 20000, rule="u")
     _check(runs, "ir_l3d40_rule_u", out)
+
+
+def test_oracle_dcgs2_cycle_is_cgs2_reordered():
+    """The oracle's lagged one-reduction CGS2 (dcgs2_cycle, this repo's
+    option) is the reference's CGS2 Arnoldi reordered: fp64 cycle residual
+    histories agree to rounding, and fp32-inner IR takes the same count."""
+    rp, ci, v = O.stencil_csr("Laplace2D", 24)
+    n = len(rp) - 1
+    b = np.ones(n)
+    _, a = O.one_cycle((rp, ci, v), None, b, np.zeros(n), 40, 1e-12)
+    _, d = O.dcgs2_cycle((rp, ci, v), None, b, np.zeros(n), 40, 1e-12)
+    assert a.steps == d.steps
+    assert np.allclose(np.log10(a.implicit), np.log10(d.implicit), atol=1e-6)
+    A = O.stencil_csr("Laplace3D", 16)
+    n = len(A[0]) - 1
+    c = O.refine(A, np.ones(n), np.zeros(n), 50, 1e-10, 20000, rule="u")
+    d = O.refine(A, np.ones(n), np.zeros(n), 50, 1e-10, 20000, rule="u", orth="dcgs2")
+    assert c.converged and d.converged and abs(c.iters - d.iters) <= 50

@@ -7,7 +7,9 @@
   * row-partitioned cycles on 2 virtual ranks (k_cycle_reg MULTI and
     k_cycle_dcgs2 MULTI) + the per-restart collectives (comm push / reduce);
   * the banded-CSR x-window SpMV (standalone and in the cycle) and the
-    device block-LU setup (k = 1, 8, 42)."""
+    device block-LU setup (k = 1, 8, 42);
+  * the lagged CGS2 over a 16-bit basis and the preset-specialised stencil
+    SpMV (k_spmv_pre)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -71,4 +73,14 @@ Mp = mk.build_gmres_poly(mk.convert_matrix(L2, P.binary32), 6, np.ones(L2.n, np.
 inner_p = mk.SolverConfig(m=30, rtol=1e-4, precision=P.binary32, max_iters=60)
 print("fused poly ir", mk.gmres_ir(L2, np.ones(L2.n), np.zeros(L2.n), mk.IrConfig(inner=inner_p, rtol=1e-10),
                                    M=Mp).total_iters)
+# round 2 (session 3): lagged CGS2 over the 16-bit basis, stencil SpMV with
+# the preset fixed at compile time (every preset, both precisions)
+for bp in ("binary16", "bfloat16"):
+    inner_dh = mk.SolverConfig(m=50, rtol=1e-4, precision=P.binary32, max_iters=100, orthogonalization="dcgs2",
+                               basis_precision=bp)
+    print("dcgs2", bp, "ir", mk.gmres_ir(A, b, np.zeros(A.n), mk.IrConfig(inner=inner_dh, rtol=1e-10)).total_iters)
+for pre, nx in (("Laplace3D", 12), ("Laplace2D", 36), ("UniFlow2D", 36), ("BentPipe2D", 36)):
+    S = mk.generate_stencil(mk.ProblemSpec(pre, nx))
+    print("spmv_pre", pre, float(mk.spmv(S, np.ones(S.n)).sum()),
+          float(mk.spmv(mk.convert_matrix(S, P.binary32), np.ones(S.n, np.float32)).sum()))
 print("sanitize ok")
