@@ -507,6 +507,7 @@ def dcgs2_cycle(A, M, b, x0, m, tol, r0=None, scale=None, cap=None, rule="n_u", 
       H[:, j-1] = [c + X0; rho]  (the append test on ||w_{j-1}||^2 = a + c.c)
       t = (b - X0.X1)/rho, tau = t/rho, c' = ([X1; t] - H X0)/rho
       q_j = (u - Q_j X0)/rho ; u' = (z - Q_j (X1 - X0 tau) - u tau)/rho
+    (the last two scaled by 1/rho, as the kernel does)
     basis16 as in one_cycle (q_j stored rounded); M must be None."""
     assert M is None, "dcgs2 restatement: identity preconditioner"
     rp, ci, vals = A
@@ -559,8 +560,9 @@ def dcgs2_cycle(A, M, b, x0, m, tol, r0=None, scale=None, cap=None, rule="n_u", 
         t = (bb - np.dot(X0, X1)) / rho
         tau = t / rho
         c = (np.append(X1, t) - H[:j + 1, :j] @ X0) / rho
-        Q[:, j] = store((u - Q[:, :j] @ X0) / rho)
-        u = (z - Q[:, :j] @ (X1 - X0 * tau) - u * tau) / rho
+        ri = dt.type(1) / rho   # the kernel scales q and u' by 1/rho (fused_dcgs2.cuh dc_phase_u)
+        Q[:, j] = store((u - Q[:, :j] @ X0) * ri)
+        u = (z - Q[:, :j] @ (X1 - X0 * tau) - u * tau) * ri
     d, err = lsq.back_solve(k)
     if err is not None:
         raise ArithmeticError("triangular breakdown", *err)

@@ -1086,32 +1086,25 @@ int mpk_spmv(const mpk_matrix *A, const void *x, void *y, void *stream) {
             }
             if constexpr (Op::kStencil) {
                 // row groups with the preset fixed at compile time
-                // (k_spmv_pre); constant-coefficient presets keep two groups'
-                // loads in flight per thread, BentPipe (double coefficient
-                // arithmetic per row) one
+                // (k_spmv_pre), one group per thread and trip: measured
+                // against the generic k_spmv (profiles/r02_spmv_pre_ab.txt)
+                // Laplace3D 200^3 55 -> 62% (fp64) and 55 -> 64% (fp32) of
+                // the copy peak, the 2-D presets unchanged; two groups per
+                // trip took 99 registers and fell to 37% in fp64
                 constexpr int R = 16 / (int)sizeof(T);
                 // StencilOp::group_ok() evaluated on the host side
                 const bool groups = op.k.preset != MPK_STRETCHED2D && op.k.nx % R == 0 && op.k.row0 % R == 0;
-                // MPK_SPMV_UG=0 (generic k_spmv) / 1 / 2 groups per trip: A/B
-                static int ug_env = -2;
-                if (ug_env == -2) {
-                    const char *e = getenv("MPK_SPMV_UG");
-                    ug_env = e ? atoi(e) : -1;
-                }
-                int ug = ug_env >= 0 ? ug_env : (op.k.preset == MPK_BENTPIPE2D ? 1 : 2);
-                if (ug > 0 && groups && ((uintptr_t)x % 16) == 0 && ((uintptr_t)y % 16) == 0) {
+                if (groups && ((uintptr_t)x % 16) == 0 && ((uintptr_t)y % 16) == 0) {
                     void (*kp)(StencilOp<T>, const T *, T *) = nullptr;
-#define MPK_PRE(P) kp = ug == 1 ? k_spmv_pre<T, P, 1> : k_spmv_pre<T, P, 2>
                     switch (op.k.preset) {
-                        case MPK_LAPLACE3D: MPK_PRE(MPK_LAPLACE3D); break;
-                        case MPK_LAPLACE2D: MPK_PRE(MPK_LAPLACE2D); break;
-                        case MPK_UNIFLOW2D: MPK_PRE(MPK_UNIFLOW2D); break;
-                        case MPK_BENTPIPE2D: MPK_PRE(MPK_BENTPIPE2D); break;
+                        case MPK_LAPLACE3D: kp = k_spmv_pre<T, MPK_LAPLACE3D, 1>; break;
+                        case MPK_LAPLACE2D: kp = k_spmv_pre<T, MPK_LAPLACE2D, 1>; break;
+                        case MPK_UNIFLOW2D: kp = k_spmv_pre<T, MPK_UNIFLOW2D, 1>; break;
+                        case MPK_BENTPIPE2D: kp = k_spmv_pre<T, MPK_BENTPIPE2D, 1>; break;
                         default: break;
                     }
-#undef MPK_PRE
                     if (kp) {
-                        int g = grid_for(kp, 0, (op.n / R + ug - 1) / ug);
+                        int g = grid_for(kp, 0, op.n / R);
                         kp<<<g, kBlock, 0, s>>>(op, (const T *)x, (T *)y);
                         return check_launch("k_spmv_pre");
                     }

@@ -46,6 +46,12 @@ __device__ __forceinline__ void dc_phase_u(const TV *V, int64_t ld, int nc, int6
     using C = RegCfg<T, TV>;
     constexpr int R = C::R;
     constexpr bool half = sizeof(TV) != sizeof(T);
+    // q and u' scale by 1/rho: one multiply per row instead of an IEEE
+    // division (~10 instructions, executed by the part-0 lanes only, which
+    // cost the 16-bit-basis stream as many issue slots as its FMAs).  The
+    // lagged CGS2 is this repo's reformulation, not the reference's
+    // operation order; oracle.dcgs2_cycle rounds the same way.
+    const T rinv = MODE == kDcUpdate2 ? RN<T>::div(T(1), rho) : T(0);
     static_assert(KU <= C::KP, "columns per part");
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane % C::G, p = lane / C::G;
@@ -134,8 +140,8 @@ __device__ __forceinline__ void dc_phase_u(const TV *V, int64_t ld, int nc, int6
                 T qv[R], un[R];
 #pragma unroll
                 for (int e = 0; e < R; ++e) {
-                    qv[e] = RN<T>::div(RN<T>::sub(uv[uu][e], s1[e]), rho);
-                    un[e] = RN<T>::div(RN<T>::sub(RN<T>::sub(zv[uu][e], s2[e]), RN<T>::mul(uv[uu][e], tau)), rho);
+                    qv[e] = RN<T>::mul(RN<T>::sub(uv[uu][e], s1[e]), rinv);
+                    un[e] = RN<T>::mul(RN<T>::sub(RN<T>::sub(zv[uu][e], s2[e]), RN<T>::mul(uv[uu][e], tau)), rinv);
                 }
                 stvrows<T, TV, R>(qout + r, qv, vs);
                 strows<T, R>(u + r, un);

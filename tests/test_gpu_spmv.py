@@ -20,8 +20,12 @@ def test_spmv_matches_reference_golden(cuda, spmv_golden):
         assert np.array_equal(mk.spmv(A32, g("x").astype(np.float32)), g("y32")), name
 
 
+# nx % 4 == 0 rows take the preset-specialised row-group kernel (k_spmv_pre)
+# in both precisions, the others the generic k_spmv's scalar rows
 @pytest.mark.parametrize("preset,nx", [("Laplace2D", 33), ("Laplace3D", 17), ("UniFlow2D", 40),
-                                       ("BentPipe2D", 70), ("Stretched2D", 31), ("Laplace2D", 2)])
+                                       ("BentPipe2D", 70), ("Stretched2D", 31), ("Laplace2D", 2),
+                                       ("Laplace3D", 16), ("Laplace2D", 64), ("BentPipe2D", 64),
+                                       ("Laplace3D", 36)])
 def test_stencil_and_csr_paths_bit_identical(cuda, preset, nx):
     A = mk.generate_stencil(mk.ProblemSpec(preset, nx))
     x = np.random.default_rng(nx).standard_normal(A.n)
