@@ -108,6 +108,12 @@ int mpk_abi_version(void);
 const char *mpk_last_error(void);
 /* number of SMs of the current device (grids are sized in multiples of it) */
 int mpk_sm_count(void);
+/* Return the L2 lines the persistent cycle kernels marked persisting (their
+ * access-policy window over the cycle's work vectors) to normal status; the
+ * solve drivers call it once at the end of a solve (no reference
+ * counterpart: B200 L2 residency control).  MPK_L2_PERSIST=0
+ * turns the window off. */
+int mpk_l2_release(void);
 
 /* ------------------------------------------------------------------ */
 /* sparse product and casts                                            */

@@ -31,7 +31,7 @@ EXPORTS = (
     "mpk_lsq_solve", "mpk_vdiv", "mpk_launch_count", "mpk_fused_prof_read", "mpk_comm_part_bytes",
     "mpk_dev_alloc", "mpk_dev_free", "mpk_ipc_get", "mpk_ipc_open", "mpk_ipc_close", "mpk_rcm_host",
     "mpk_last_cycle_kernel", "mpk_can_access_peer", "mpk_comm_push_rows", "mpk_comm_reduce_ctl",
-    "mpk_block_lu", "mpk_stencil_assemble", "mpk_stencil_assemble_ws_bytes",
+    "mpk_block_lu", "mpk_stencil_assemble", "mpk_stencil_assemble_ws_bytes", "mpk_l2_release",
 )
 MAX_RANKS = 8
 
@@ -125,6 +125,7 @@ _SIGS = {
 _SIGS["mpk_launch_count"] = (_I64, [])
 _SIGS["mpk_last_cycle_kernel"] = (ctypes.c_char_p, [])
 _SIGS["mpk_can_access_peer"] = (_I32, [_I32, _I32])
+_SIGS["mpk_l2_release"] = (_I32, [])
 _SIGS["mpk_comm_push_rows"] = (_I32, [ctypes.c_void_p, _I32, _I64, _P, _P])
 _SIGS["mpk_comm_reduce_ctl"] = (_I32, [ctypes.c_void_p, _I32, _P, _I32, _I32, _P])
 _SIGS["mpk_fused_prof_read"] = (_I32, [ctypes.POINTER(ctypes.c_uint64), _I32])

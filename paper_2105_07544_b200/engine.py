@@ -178,6 +178,25 @@ class CycleWorkspace:
         return D.to_host(raw[:k, : k + 1].t()).astype(np.float64)
 
 
+def releases_l2(fn):
+    """Solve-driver decorator: after the solve, return the L2 lines the cycle
+    kernels' access-policy window marked persisting to normal status
+    (mpk_l2_release), so the set-aside is free for whatever runs next."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapper(*args, **kwargs):
+        try:
+            return fn(*args, **kwargs)
+        finally:
+            try:
+                D.lib().mpk_l2_release()
+            except _lib.NativeUnavailable:
+                pass
+
+    return wrapper
+
+
 def sqrt_in(prec: Precision, v: float) -> float:
     """float(np.sqrt(v)) with the square root taken in prec (norm2's rounding)."""
     return float(np.sqrt(prec.dtype.type(v)))

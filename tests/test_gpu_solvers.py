@@ -234,3 +234,31 @@ def test_run_to_run_bit_identical(cuda):
     g1 = gm(A, b, m=50, rtol=1e-10)
     g2 = gm(A, b, m=50, rtol=1e-10)
     assert g1.x.tobytes() == g2.x.tobytes() and g1.total_iters == g2.total_iters
+
+
+def test_l2_window_release_and_env_off(cuda):
+    """The cycle kernels launch with an L2 access-policy window over their
+    work vectors; mpk_l2_release returns the persisting lines to normal after
+    a solve.  With MPK_L2_PERSIST=0 (a fresh process) the solve is the same
+    bit for bit: the window changes cache residency, not arithmetic."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    from paper_2105_07544_b200 import _lib
+
+    assert _lib.load().mpk_l2_release() == 0
+    code = ("import sys, json, numpy as np; sys.path.insert(0, %r); import paper_2105_07544_b200 as mk; "
+            "A = mk.generate_stencil(mk.ProblemSpec('Laplace3D', 24)); "
+            "inner = mk.SolverConfig(m=50, rtol=1e-4, precision=mk.Precision.binary32); "
+            "r = mk.gmres_ir(A, np.ones(A.n), np.zeros(A.n), mk.IrConfig(inner=inner, rtol=1e-10)); "
+            "print(json.dumps([r.total_iters, r.x.tobytes().hex()[:4096], r.final_explicit_relres]))"
+            % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    outs = []
+    for flag in ("1", "0"):
+        env = dict(os.environ, MPK_L2_PERSIST=flag)
+        p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+        assert p.returncode == 0, p.stderr
+        outs.append(json.loads(p.stdout.strip().splitlines()[-1]))
+    assert outs[0] == outs[1]
