@@ -9,12 +9,22 @@ peak = 6539.5
 def bench(name, A, reps=20):
     for prec in (P.binary64, P.binary32):
         B = mk.convert_matrix(A, prec)
-        x = torch.randn(A.n, dtype=prec.torch_dtype, device="cuda"); y = torch.empty_like(x)
+        sv0 = 4 if prec is P.binary32 else 8
+        npair = max(1, min(20, -(-384 * 2**20 // (2 * sv0 * A.n))))   # vectors never L2-resident across launches
+        pairs = [(torch.randn(A.n, dtype=prec.torch_dtype, device="cuda"),
+                  torch.empty(A.n, dtype=prec.torch_dtype, device="cuda")) for _ in range(npair)]
+        x, y = pairs[0]
         spmv_into(B, x, y); torch.cuda.synchronize()
+        # captured in a CUDA graph: a Python launch loop is host-bound for short kernels
+        side = torch.cuda.Stream(); side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side): spmv_into(B, x, y)
+        torch.cuda.current_stream().wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for i in range(reps): spmv_into(B, *pairs[i % npair])
+        g.replay(); torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(reps): spmv_into(B, x, y)
-        e1.record(); torch.cuda.synchronize()
+        e0.record(); g.replay(); e1.record(); torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps
         sv = 4 if prec is P.binary32 else 8
         if B.stencil is not None and B.use_stencil:
