@@ -624,6 +624,23 @@ size_t l2_persist_bytes() {
     return aside;
 }
 
+// Resident CTAs per SM of a persistent cycle kernel at `smem` bytes of
+// dynamic shared memory, cached per (kernel, smem): the occupancy query costs
+// tens of microseconds of host time, and it used to run before every cycle
+// launch (on the GPU-idle path between refinements).
+int coop_per_sm(const void *kern, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::pair<const void *, size_t>, int> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_pair(kern, smem);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFB, smem);
+    cache[key] = per_sm;
+    return per_sm;
+}
+
 // Cooperative launch of a persistent cycle kernel, with the L2 window over
 // [win, win + win_bytes) when persistence is available.
 cudaError_t launch_cycle_coop(const void *kern, int grid, size_t smem, cudaStream_t s, void **args, const void *win,
@@ -686,9 +703,7 @@ int launch_fused_reg(const Op &op, const mpk_cycle_desc *d, int cap, double tf, 
         }
         attr_set[vi] = smem;
     }
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFB, smem);
-    if (per_sm < 1) return fail(MPK_ELAUNCH, "register cycle kernel does not fit on an SM");
+    if (coop_per_sm((const void *)kern, smem) < 1) return fail(MPK_ELAUNCH, "register cycle kernel does not fit on an SM");
     int grid = sm_count_cached();
     if (grid > kFMaxCtas) grid = kFMaxCtas;
     if (d->nranks <= 1) grid = fused_grid(grid, d->n);   // ranks must agree on the CTA count (partial columns)
@@ -811,9 +826,7 @@ int launch_dcgs2(const Op &op, const mpk_cycle_desc *d, int cap, double tf, doub
         }
         attr_set[mi] = smem;
     }
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFB, smem);
-    if (per_sm < 1) return fail(MPK_ELAUNCH, "dcgs2 cycle kernel does not fit on an SM");
+    if (coop_per_sm((const void *)kern, smem) < 1) return fail(MPK_ELAUNCH, "dcgs2 cycle kernel does not fit on an SM");
     int grid = sm_count_cached();
     if (grid > 160) grid = 160;   // cross_reduce fast path
     if (d->nranks <= 1) grid = fused_grid(grid, d->n);
