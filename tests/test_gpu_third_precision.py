@@ -86,3 +86,18 @@ def test_lagged_cgs2_over_16bit_basis_vs_oracle(cuda, preset, nx, basis):
                    basis16=True if basis == "binary16" else "bfloat16")
     assert rep.converged and ref.converged and rep.final_explicit_relres <= 1e-10
     assert abs(rep.total_iters - ref.iters) <= 50, (rep.total_iters, ref.iters)
+
+
+def test_lagged_cgs2_over_binary16_basis_with_jacobi1_csr(cuda):
+    """The lagged CGS2 over the binary16 basis on a CSR operator with a
+    diagonal (block-Jacobi k = 1) right preconditioner: k_cycle_dcgs2<float,
+    CsrOp<float>, false, __half> with z = q_0 / a_ii from the stored q_0."""
+    A = mk.synthetic_irregular(20000, signs="negative", dominance=1.001, shift=1e-3, far_frac=0.01, band=200)
+    M = mk.build_block_jacobi(mk.convert_matrix(A, P.binary32), 1)
+    inner = mk.SolverConfig(m=50, rtol=1e-4, precision=P.binary32, max_iters=20000, breakdown_rule="u",
+                            orthogonalization="dcgs2", basis_precision="binary16")
+    rep = mk.gmres_ir(A, np.ones(A.n), np.zeros(A.n), mk.IrConfig(inner=inner, rtol=1e-10), M=M)
+    assert _lib.last_cycle_kernel() == "k_cycle_dcgs2/half"
+    base = ir(A, "working", rule="u", M=M)
+    assert rep.converged and rep.final_explicit_relres <= 1e-10
+    assert rep.total_iters <= 1.5 * base.total_iters + 50, (rep.total_iters, base.total_iters)
